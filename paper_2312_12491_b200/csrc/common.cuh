@@ -1,0 +1,59 @@
+// Shared helpers for the sm_100a streaming-denoise library.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "stagger_b200.h"
+
+namespace sdx {
+
+// Status-carrying exception used inside the library; the C-ABI layer turns it
+// into an SDX_* return code plus a thread-local message.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void raise(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        raise(SDX_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file +
+                                  ":" + std::to_string(line) + ")");
+}
+
+#define SDX_CUDA(x) ::sdx::cuda_check((x), #x, __FILE__, __LINE__)
+#define SDX_LAUNCH_CHECK() ::sdx::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+constexpr int kMaxSteps = 64;     // n_steps upper bound for device slot tables
+constexpr int kSmCount = 148;     // B200
+
+template <class T>
+inline T* dev_alloc(size_t count) {
+    if (count == 0) return nullptr;
+    void* p = nullptr;
+    SDX_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+inline void dev_free(void* p) {
+    if (p) cudaFree(p);
+}
+
+// Per-step scalar table, computed on the host in fp64 from build_schedule /
+// lcm_coefficients (schedule.cpp:29-107) and consumed in fp64 on device.
+struct StepScalars {
+    double sa, sb;          // sqrt(alpha), sqrt(beta)
+    double c_skip, c_out;   // LCM output parameterisation at this step
+    double an_scale;        // analytic denoiser: sqrt(beta) / (alpha*var + beta)
+    double beta;            // raw beta (R-CFG falls back to eps_cond when beta <= 0)
+    double alpha;
+    int tau;
+    int pad;
+};
+
+}  // namespace sdx

@@ -1,0 +1,790 @@
+// Host runtime: device-state owners and the host mirror of the reference's
+// engine / pipeline bookkeeping.  See runtime.cuh.
+#include "runtime.cuh"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+
+namespace sdx {
+
+// ---------------------------------------------------------------------------
+// EngineMirror — StreamBatchEngine bookkeeping (engine.cpp:53-211)
+// ---------------------------------------------------------------------------
+
+void EngineMirror::check_ingest(int64_t seq) const {
+    if (seq <= last_seq_) raise(SDX_INVALID_ARGUMENT, "ingest: seq ids must strictly increase");
+    for (const auto& f : inflight_)
+        if (f.step == 0) raise(SDX_LOGIC_ERROR, "ingest: step-0 slot already occupied, tick first");
+}
+
+void EngineMirror::ingest(int64_t seq) {
+    inflight_.push_back(Frame{seq, 0, ticks_});
+    last_seq_ = seq;
+    pending_ = true;
+    pending_seq_ = seq;
+}
+
+EngineMirror::TickOut EngineMirror::tick() {
+    if (inflight_.empty()) raise(SDX_LOGIC_ERROR, "tick: no in-flight frames");
+    TickOut out;
+    const uint64_t b = inflight_.size();
+    out.rows = b;
+    if (guidance_ == SDX_GUIDANCE_CFG) out.rows += b;
+    if (guidance_ == SDX_GUIDANCE_ONETIME_NEGATIVE && pending_) out.rows += 1;
+    ticks_ += 1;
+    calls += 1;
+    evals += out.rows;
+    size_t emit_index = inflight_.size();
+    for (size_t i = 0; i < inflight_.size(); ++i) {
+        auto& f = inflight_[i];
+        f.step += 1;
+        if (f.step == n_) {
+            out.emitted = true;
+            out.seq = f.seq;
+            out.ingest_tick = f.ingest_tick;
+            out.emit_tick = ticks_;
+            emit_index = i;
+        }
+    }
+    if (emit_index < inflight_.size()) inflight_.erase(inflight_.begin() + static_cast<long>(emit_index));
+    pending_ = false;
+    pending_seq_ = -1;
+    return out;
+}
+
+std::vector<int> EngineMirror::step_indices() const {
+    std::vector<int> v;
+    for (const auto& f : inflight_) v.push_back(f.step);
+    std::sort(v.begin(), v.end());
+    return v;
+}
+
+int64_t EngineMirror::min_inflight_seq() const {
+    int64_t m = INT64_MAX;
+    for (const auto& f : inflight_) m = std::min(m, f.seq);
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// step table + device engine
+// ---------------------------------------------------------------------------
+
+std::vector<StepScalars> make_step_table(const sdx_step* steps, int n, int lcm_mode, double var) {
+    std::vector<StepScalars> t(static_cast<size_t>(n) + 1);
+    for (int i = 0; i <= n; ++i) {
+        const bool term = i == n;
+        const int tau = term ? 0 : steps[i].tau;
+        const double alpha = term ? 1.0 : steps[i].alpha;
+        const double beta = term ? 0.0 : steps[i].beta;
+        StepScalars& s = t[static_cast<size_t>(i)];
+        s.tau = tau;
+        s.alpha = alpha;
+        s.beta = beta;
+        s.sa = std::sqrt(alpha);
+        s.sb = std::sqrt(beta);
+        // lcm_coefficients (schedule.cpp:80-89), sigma_data 0.5, s 10
+        if (lcm_mode == SDX_LCM_BOUNDARY_APPROX) {
+            s.c_skip = tau == 0 ? 1.0 : 0.0;
+            s.c_out = tau == 0 ? 0.0 : 1.0;
+        } else {
+            const double st = 10.0 * tau;
+            const double sig2 = 0.25;
+            s.c_skip = sig2 / (st * st + sig2);
+            s.c_out = 0.5 * st / std::sqrt(sig2 + st * st);
+        }
+        s.an_scale = std::sqrt(beta) / (alpha * var + beta);
+        s.pad = 0;
+    }
+    return t;
+}
+
+void DeviceEngine::init(int S_, int n_, long long d_, int guidance_, double gamma_, double delta_,
+                        const std::vector<StepScalars>& table, bool per_slot_cond_) {
+    S = S_;
+    n = n_;
+    d = d_;
+    guidance = guidance_;
+    gamma = gamma_;
+    delta = delta_;
+    per_slot_cond = per_slot_cond_;
+    const size_t sn = static_cast<size_t>(S) * n;
+    const size_t snd = sn * static_cast<size_t>(d);
+    tbl = dev_alloc<StepScalars>(table.size());
+    SDX_CUDA(cudaMemcpy(tbl, table.data(), sizeof(StepScalars) * table.size(), cudaMemcpyHostToDevice));
+    x_cur = dev_alloc<float>(snd);
+    x0 = dev_alloc<float>(snd);
+    if (guidance == SDX_GUIDANCE_ONETIME_NEGATIVE) x0ref = dev_alloc<float>(snd);
+    eps_cached = dev_alloc<float>(snd);
+    cond = dev_alloc<float>(per_slot_cond ? snd : static_cast<size_t>(S) * d);
+    if (guidance == SDX_GUIDANCE_CFG || guidance == SDX_GUIDANCE_ONETIME_NEGATIVE)
+        neg = dev_alloc<float>(static_cast<size_t>(S) * d);
+    emitted = dev_alloc<float>(static_cast<size_t>(S) * d);
+    SDX_CUDA(cudaMemset(x_cur, 0, snd * sizeof(float)));
+    SDX_CUDA(cudaMemset(x0, 0, snd * sizeof(float)));
+    SDX_CUDA(cudaMemset(emitted, 0, static_cast<size_t>(S) * d * sizeof(float)));
+    ctl = dev_alloc<StreamCtl>(static_cast<size_t>(S));
+    std::vector<StreamCtl> h(static_cast<size_t>(S));
+    for (auto& c : h) {
+        std::memset(&c, 0, sizeof c);
+        c.last_seq = -1;
+        c.ingest_slot = -1;
+        c.emit_slot = -1;
+        c.emit_seq = -1;
+        c.mti = 312;
+        c.decision = SDX_GATE_PROCESS;
+        for (auto& sl : c.slot) sl.seq = -1;
+    }
+    SDX_CUDA(cudaMemcpy(ctl, h.data(), sizeof(StreamCtl) * h.size(), cudaMemcpyHostToDevice));
+    const int rmax = S * 2 * n + S;
+    rows = dev_alloc<RowDesc>(static_cast<size_t>(rmax));
+    n_rows = dev_alloc<int>(1);
+    slot_row_c = dev_alloc<int>(static_cast<size_t>(S) * kMaxSteps);
+    slot_row_n = dev_alloc<int>(static_cast<size_t>(S) * kMaxSteps);
+    log = dev_alloc<LogEntry>(static_cast<size_t>(S));
+}
+
+void DeviceEngine::release() {
+    for (void* p : {static_cast<void*>(tbl), static_cast<void*>(x_cur), static_cast<void*>(x0),
+                    static_cast<void*>(x0ref), static_cast<void*>(eps_cached), static_cast<void*>(cond),
+                    static_cast<void*>(neg), static_cast<void*>(emitted), static_cast<void*>(ctl),
+                    static_cast<void*>(rows), static_cast<void*>(n_rows), static_cast<void*>(slot_row_c),
+                    static_cast<void*>(slot_row_n), static_cast<void*>(log)})
+        dev_free(p);
+    tbl = nullptr;
+}
+
+StepArgs DeviceEngine::step_args() const {
+    StepArgs a{};
+    a.n = n;
+    a.d = d;
+    a.guidance = guidance;
+    a.gamma = gamma;
+    a.delta = delta;
+    a.tbl = tbl;
+    a.x_cur = x_cur;
+    a.x0 = x0;
+    a.x0ref = x0ref;
+    a.eps_cached = eps_cached;
+    a.cond = cond;
+    a.cond_stream_stride = per_slot_cond ? static_cast<long long>(n) * d : d;
+    a.cond_slot_stride = per_slot_cond ? d : 0;
+    a.neg = neg;
+    a.eps_ext = nullptr;
+    a.eps_ext_stride = 0;
+    a.slot_row_c = slot_row_c;
+    a.slot_row_n = slot_row_n;
+    a.emitted = emitted;
+    a.ctl = ctl;
+    return a;
+}
+
+static void upload_f32(float* dst, const double* src, size_t count, cudaStream_t st) {
+    std::vector<float> tmp(count);
+    for (size_t i = 0; i < count; ++i) tmp[i] = static_cast<float>(src[i]);
+    // pageable source: the call returns once the bytes are staged
+    SDX_CUDA(cudaMemcpyAsync(dst, tmp.data(), count * sizeof(float), cudaMemcpyHostToDevice, st));
+    SDX_CUDA(cudaStreamSynchronize(st));
+}
+
+static std::string config_errors(const sdx_config& c) {
+    // validate_config (core.cpp:26-60); all violations joined (core.cpp:62-69)
+    std::vector<std::string> e;
+    if (c.n_steps < 1) e.push_back("n_steps must be >= 1");
+    if (!(c.eta >= 0.0 && c.eta < 1.0)) e.push_back("eta out of range: must lie in [0,1) so 1-eta stays positive");
+    if (!(c.gamma >= 0.0)) e.push_back("gamma must be >= 0");
+    if (!(c.delta >= 0.0 && c.delta <= 1.0)) e.push_back("delta must lie in [0,1]");
+    if (c.d_latent < 1) e.push_back("d_latent must be >= 1");
+    if (c.t_grid < 1) e.push_back("t_grid must be >= 1");
+    if (c.n_steps > c.t_grid) e.push_back("n_steps must not exceed t_grid");
+    if (!(c.entry_strength > 0.0 && c.entry_strength <= 1.0)) e.push_back("entry_strength must lie in (0,1]");
+    if (c.backend != SDX_BACKEND_ANALYTIC && c.backend != SDX_BACKEND_UNET)
+        e.push_back("backend must be analytic or unet");
+    if (!(c.data_variance > 0.0)) e.push_back("data_variance must be > 0");
+    if (c.lcm_mode != SDX_LCM_EXACT && c.lcm_mode != SDX_LCM_BOUNDARY_APPROX)
+        e.push_back("lcm_mode must be \"exact\" or \"boundary_approx\"");
+    if (c.codec != SDX_CODEC_IDENTITY && c.codec != SDX_CODEC_TAESD) e.push_back("codec must be identity or taesd");
+    if (c.queue_capacity < 1) e.push_back("queue_capacity must be >= 1");
+    if (c.n_steps > kMaxSteps) e.push_back("n_steps exceeds the device slot table (64)");
+    if (e.empty()) return {};
+    std::ostringstream o;
+    o << "invalid config:";
+    for (const auto& m : e) o << "\n  - " << m;
+    return o.str();
+}
+
+// ---------------------------------------------------------------------------
+// Engine
+// ---------------------------------------------------------------------------
+
+Engine::Engine(const sdx_config& cfg, const sdx_step* steps, int n, const double* eps_cached,
+               const double* neg, int device)
+    : cfg_(cfg), device_(device), mirror_(cfg.n_steps, cfg.guidance_mode) {
+    const std::string errs = config_errors(cfg);
+    if (!errs.empty()) raise(SDX_INVALID_ARGUMENT, errs);
+    if (cfg.cross_frame_attention) raise(SDX_UNSUPPORTED, "cross_frame_attention is not built (SURVEY §8f)");
+    if (cfg.backend != SDX_BACKEND_ANALYTIC)
+        raise(SDX_UNSUPPORTED, "engine API: the UNet backend runs through sdx_pipeline");
+    if (n != cfg.n_steps) raise(SDX_INVALID_ARGUMENT, "StreamBatchEngine: schedule length != n_steps");
+    if (!eps_cached) raise(SDX_INVALID_ARGUMENT, "StreamBatchEngine: noise cache length != n_steps");
+    const bool needs_neg = cfg.guidance_mode == SDX_GUIDANCE_CFG || cfg.guidance_mode == SDX_GUIDANCE_ONETIME_NEGATIVE;
+    if (needs_neg && !neg) raise(SDX_INVALID_ARGUMENT, "StreamBatchEngine: guidance mode requires negative_cond");
+    for (int i = 0; i < n; ++i)
+        if (!(steps[i].alpha > 0.0)) raise(SDX_INVALID_ARGUMENT, "predict_x0: singular step (alpha = 0)");
+    SDX_CUDA(cudaSetDevice(device_));
+    SDX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    SDX_CUDA(cudaEventCreate(&ev0_));
+    SDX_CUDA(cudaEventCreate(&ev1_));
+    const auto table = make_step_table(steps, n, cfg.lcm_mode, cfg.data_variance);
+    dev_.init(1, n, cfg.d_latent, cfg.guidance_mode, cfg.gamma, cfg.delta, table, /*per_slot_cond=*/true);
+    const size_t d = static_cast<size_t>(cfg.d_latent);
+    upload_f32(dev_.eps_cached, eps_cached, static_cast<size_t>(n) * d, stream_);
+    if (dev_.neg && neg) upload_f32(dev_.neg, neg, d, stream_);
+    slot_cond_.resize(static_cast<size_t>(n));
+    SDX_CUDA(cudaMallocHost(&h_stage_, sizeof(float) * d));
+    SDX_CUDA(cudaMallocHost(&h_log_, sizeof(LogEntry)));
+}
+
+Engine::~Engine() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    dev_.release();
+    if (h_stage_) cudaFreeHost(h_stage_);
+    if (h_log_) cudaFreeHost(h_log_);
+    if (ev0_) cudaEventDestroy(ev0_);
+    if (ev1_) cudaEventDestroy(ev1_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::ingest(int64_t seq, const double* x0, const double* cond) {
+    const size_t d = static_cast<size_t>(cfg_.d_latent);
+    if (!x0 || !cond) raise(SDX_INVALID_ARGUMENT, "ingest: latent length != d_latent");
+    for (size_t i = 0; i < d; ++i)
+        if (!std::isfinite(x0[i])) raise(SDX_INVALID_ARGUMENT, "ingest: non-finite latent");
+    mirror_.check_ingest(seq);
+    SDX_CUDA(cudaSetDevice(device_));
+    const int slot = static_cast<int>(mirror_.ticks() % cfg_.n_steps);
+    upload_f32(dev_.x0 + static_cast<size_t>(slot) * d, x0, d, stream_);
+    auto& last = slot_cond_[static_cast<size_t>(slot)];
+    bool same = last.size() == d;
+    for (size_t i = 0; same && i < d; ++i) same = last[i] == static_cast<float>(cond[i]);
+    if (!same) {
+        last.resize(d);
+        for (size_t i = 0; i < d; ++i) last[i] = static_cast<float>(cond[i]);
+        SDX_CUDA(cudaMemcpyAsync(dev_.cond + static_cast<size_t>(slot) * d, last.data(), d * sizeof(float),
+                                 cudaMemcpyHostToDevice, stream_));
+    }
+    mirror_.ingest(seq);
+}
+
+sdx_tick_result Engine::tick(double* x0_hat) {
+    const bool pend = mirror_.pending_ingest();
+    const int64_t pseq = mirror_.pending_seq();
+    const auto t = mirror_.tick();  // throws logic_error on an empty engine
+    SDX_CUDA(cudaSetDevice(device_));
+    const int n = cfg_.n_steps;
+    SDX_CUDA(cudaEventRecord(ev0_, stream_));
+    launch_ctl_begin(dev_.ctl, 1, n, cfg_.guidance_mode, kIngestHost, pend ? pseq : -1, 0, nullptr, nullptr,
+                     nullptr, nullptr, stream_);
+    launch_step(dev_.step_args(), 1, stream_);
+    launch_ctl_end(dev_.ctl, 1, n, cfg_.guidance_mode, dev_.log, 0, stream_);
+    SDX_CUDA(cudaEventRecord(ev1_, stream_));
+    timed_ = true;
+    sdx_tick_result r{};
+    r.emitted_seq = -1;
+    r.denoiser_calls = 1;
+    r.element_evals = t.rows;
+    if (t.emitted) {
+        const size_t d = static_cast<size_t>(cfg_.d_latent);
+        SDX_CUDA(cudaMemcpyAsync(h_log_, dev_.log, sizeof(LogEntry), cudaMemcpyDeviceToHost, stream_));
+        SDX_CUDA(cudaMemcpyAsync(h_stage_, dev_.emitted, d * sizeof(float), cudaMemcpyDeviceToHost, stream_));
+        SDX_CUDA(cudaStreamSynchronize(stream_));
+        if (h_log_->emit_seq != t.seq) raise(SDX_RUNTIME_ERROR, "device/host engine mirror diverged");
+        if (h_log_->nonfinite) raise(SDX_RUNTIME_ERROR, "tick: non-finite latent at emission");
+        if (x0_hat)
+            for (size_t i = 0; i < d; ++i) x0_hat[i] = static_cast<double>(h_stage_[i]);
+        r.emitted_seq = t.seq;
+        r.ingest_tick = t.ingest_tick;
+        r.emit_tick = t.emit_tick;
+    }
+    float ms = 0.f;
+    SDX_CUDA(cudaEventSynchronize(ev1_));
+    SDX_CUDA(cudaEventElapsedTime(&ms, ev0_, ev1_));
+    last_ms_ = ms;
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// MT19937-64 seeding (std::mt19937_64)
+// ---------------------------------------------------------------------------
+
+void mt_seed_words(uint64_t seed, unsigned long long* mt) {
+    mt[0] = seed;
+    for (int i = 1; i < 312; ++i) mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + i;
+}
+
+// ---------------------------------------------------------------------------
+// Ssf
+// ---------------------------------------------------------------------------
+
+Ssf::Ssf(double eta, uint64_t seed, int max_skip, int64_t frame_bytes, int device)
+    : eta_(eta), max_skip_(max_skip), D_(frame_bytes), device_(device) {
+    if (!(eta >= 0.0 && eta < 1.0)) raise(SDX_INVALID_ARGUMENT, "SsfState: eta must lie in [0,1)");
+    if (frame_bytes < 1) raise(SDX_INVALID_ARGUMENT, "SsfState: frame_bytes must be >= 1");
+    SDX_CUDA(cudaSetDevice(device_));
+    SDX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    const int64_t pad = (D_ + 15) / 16 * 16;
+    batch_ = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(64, (64LL << 20) / pad)));
+    d_frames_ = dev_alloc<uint8_t>(static_cast<size_t>(pad) * batch_);
+    d_ref_ = dev_alloc<uint8_t>(static_cast<size_t>(pad));
+    SDX_CUDA(cudaMemset(d_ref_, 0, static_cast<size_t>(pad)));
+    ctl_ = dev_alloc<StreamCtl>(1);
+    StreamCtl h;
+    std::memset(&h, 0, sizeof h);
+    h.mti = 312;
+    h.decision = SDX_GATE_PROCESS;
+    for (auto& sl : h.slot) sl.seq = -1;
+    SDX_CUDA(cudaMemcpy(ctl_, &h, sizeof h, cudaMemcpyHostToDevice));
+    mt_ = dev_alloc<unsigned long long>(312);
+    unsigned long long words[312];
+    mt_seed_words(seed, words);
+    SDX_CUDA(cudaMemcpy(mt_, words, sizeof words, cudaMemcpyHostToDevice));
+    dec_ = dev_alloc<int>(static_cast<size_t>(batch_));
+    sims_ = dev_alloc<double>(static_cast<size_t>(batch_));
+}
+
+Ssf::~Ssf() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    dev_free(d_frames_);
+    dev_free(d_ref_);
+    dev_free(ctl_);
+    dev_free(mt_);
+    dev_free(dec_);
+    dev_free(sims_);
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Ssf::gate(const uint8_t* frames, int nframes, int* decisions, double* sims) {
+    SDX_CUDA(cudaSetDevice(device_));
+    const int64_t pad = (D_ + 15) / 16 * 16;
+    std::vector<int> hd(static_cast<size_t>(batch_));
+    std::vector<double> hs(static_cast<size_t>(batch_));
+    for (int base = 0; base < nframes; base += batch_) {
+        const int cnt = std::min(batch_, nframes - base);
+        for (int i = 0; i < cnt; ++i)
+            SDX_CUDA(cudaMemcpyAsync(d_frames_ + static_cast<size_t>(i) * pad,
+                                     frames + static_cast<size_t>(base + i) * D_, static_cast<size_t>(D_),
+                                     cudaMemcpyHostToDevice, stream_));
+        for (int i = 0; i < cnt; ++i) {
+            SsfArgs a{};
+            a.frames = d_frames_ + static_cast<size_t>(i) * pad;
+            a.frame_stride = pad;
+            a.ref = d_ref_;
+            a.D = D_;
+            a.eta = eta_;
+            a.max_skip = max_skip_;
+            a.ctl = ctl_;
+            a.mt_state = mt_;
+            a.dec_out = dec_ + i;
+            a.sim_out = sims_ + i;
+            launch_ssf_reduce(a, 1, stream_);
+            CommitArgs ca{};
+            ca.frames = a.frames;
+            ca.frame_stride = pad;
+            ca.ref = d_ref_;
+            ca.D = D_;
+            ca.x0 = nullptr;
+            ca.ctl = ctl_;
+            launch_commit_encode(ca, 1, stream_);
+        }
+        SDX_CUDA(cudaMemcpyAsync(hd.data(), dec_, sizeof(int) * cnt, cudaMemcpyDeviceToHost, stream_));
+        SDX_CUDA(cudaMemcpyAsync(hs.data(), sims_, sizeof(double) * cnt, cudaMemcpyDeviceToHost, stream_));
+        SDX_CUDA(cudaStreamSynchronize(stream_));
+        for (int i = 0; i < cnt; ++i) {
+            examined_ += 1;
+            if (hd[static_cast<size_t>(i)] == SDX_GATE_SKIP) skipped_ += 1;
+            if (decisions) decisions[base + i] = hd[static_cast<size_t>(i)];
+            if (sims) sims[base + i] = hs[static_cast<size_t>(i)];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pipeline
+// ---------------------------------------------------------------------------
+
+Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const double* eps_cached,
+                   const double* cond, const double* neg, int device)
+    : cfg_(cfg), S_(cfg.n_streams), n_(cfg.engine.n_steps), K_(std::max(2, cfg.ring_depth)),
+      D_(cfg.frame_bytes), d_(cfg.engine.d_latent), device_(device) {
+    const auto& e = cfg.engine;
+    const std::string errs = config_errors(e);
+    if (!errs.empty()) raise(SDX_INVALID_ARGUMENT, errs);
+    if (e.cross_frame_attention) raise(SDX_UNSUPPORTED, "cross_frame_attention is not built (SURVEY §8f)");
+    if (S_ < 1 || S_ > 1024) raise(SDX_INVALID_ARGUMENT, "n_streams must lie in [1,1024]");
+    if (e.backend != SDX_BACKEND_ANALYTIC) raise(SDX_UNSUPPORTED, "UNet backend not available in this build");
+    if (e.codec != SDX_CODEC_IDENTITY) raise(SDX_UNSUPPORTED, "TAESD codec not available in this build");
+    if (e.codec == SDX_CODEC_IDENTITY && D_ != d_)
+        raise(SDX_INVALID_ARGUMENT, "LatentCodec::encode: dim mismatch");
+    const bool needs_neg = e.guidance_mode == SDX_GUIDANCE_CFG || e.guidance_mode == SDX_GUIDANCE_ONETIME_NEGATIVE;
+    if (needs_neg && !neg)
+        raise(SDX_INVALID_ARGUMENT,
+              "invalid config:\n  - negative_condition is required for cfg/onetime_negative modes");
+    for (int i = 0; i < n_; ++i)
+        if (!(steps[i].alpha > 0.0)) raise(SDX_INVALID_ARGUMENT, "predict_x0: singular step (alpha = 0)");
+    SDX_CUDA(cudaSetDevice(device_));
+    SDX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    SDX_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+    const auto table = make_step_table(steps, n_, e.lcm_mode, e.data_variance);
+    dev_.init(S_, n_, d_, e.guidance_mode, e.gamma, e.delta, table, /*per_slot_cond=*/false);
+    const size_t d = static_cast<size_t>(d_);
+    upload_f32(dev_.eps_cached, eps_cached, static_cast<size_t>(S_) * n_ * d, stream_);
+    upload_f32(dev_.cond, cond, static_cast<size_t>(S_) * d, stream_);
+    if (dev_.neg && neg) upload_f32(dev_.neg, neg, static_cast<size_t>(S_) * d, stream_);
+    pad_ = (D_ + 15) / 16 * 16;
+    d_in_ = dev_alloc<uint8_t>(static_cast<size_t>(K_) * S_ * pad_);
+    if (e.ssf_enabled) {
+        d_ref_ = dev_alloc<uint8_t>(static_cast<size_t>(S_) * pad_);
+        SDX_CUDA(cudaMemset(d_ref_, 0, static_cast<size_t>(S_) * pad_));
+        mt_ = dev_alloc<unsigned long long>(static_cast<size_t>(S_) * 312);
+        std::vector<unsigned long long> words(static_cast<size_t>(S_) * 312);
+        for (int s = 0; s < S_; ++s) {
+            // per-stream SSF Rng(derive_seed(seed_s, kStreamSsf)), pipeline.cpp:166-167
+            uint64_t z = (e.seed + static_cast<uint64_t>(s)) + 0x9e3779b97f4a7c15ULL * (2 + 1);
+            z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+            z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+            z = z ^ (z >> 31);
+            mt_seed_words(z, words.data() + static_cast<size_t>(s) * 312);
+        }
+        SDX_CUDA(cudaMemcpy(mt_, words.data(), words.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
+    }
+    out_bytes_ = d * sizeof(float);
+    SDX_CUDA(cudaMallocHost(&h_in_, static_cast<size_t>(K_) * S_ * D_));
+    SDX_CUDA(cudaMallocHost(&h_out_, static_cast<size_t>(K_) * S_ * out_bytes_));
+    SDX_CUDA(cudaMallocHost(&h_log_, static_cast<size_t>(K_) * S_ * sizeof(LogEntry)));
+    done_.resize(static_cast<size_t>(K_));
+    h2d_.resize(static_cast<size_t>(K_));
+    for (int k = 0; k < K_; ++k) {
+        SDX_CUDA(cudaEventCreateWithFlags(&done_[static_cast<size_t>(k)], cudaEventDisableTiming));
+        SDX_CUDA(cudaEventCreateWithFlags(&h2d_[static_cast<size_t>(k)], cudaEventDisableTiming));
+    }
+    SDX_CUDA(cudaEventCreate(&t0_));
+    SDX_CUDA(cudaEventCreate(&t1_));
+    st_.resize(static_cast<size_t>(S_));
+    for (auto& h : st_) h.eng = std::make_unique<EngineMirror>(n_, e.guidance_mode);
+}
+
+Pipeline::~Pipeline() {
+    cudaSetDevice(device_);
+    if (stream_) cudaStreamSynchronize(stream_);
+    if (copy_) cudaStreamSynchronize(copy_);
+    dev_.release();
+    dev_free(d_in_);
+    dev_free(d_ref_);
+    dev_free(mt_);
+    if (h_in_) cudaFreeHost(h_in_);
+    if (h_out_) cudaFreeHost(h_out_);
+    if (h_log_) cudaFreeHost(h_log_);
+    for (auto ev : done_) cudaEventDestroy(ev);
+    for (auto ev : h2d_) cudaEventDestroy(ev);
+    if (t0_) cudaEventDestroy(t0_);
+    if (t1_) cudaEventDestroy(t1_);
+    if (stream_) cudaStreamDestroy(stream_);
+    if (copy_) cudaStreamDestroy(copy_);
+}
+
+void Pipeline::launch_iteration(int k, bool frame_present) {
+    const auto& e = cfg_.engine;
+    uint8_t* frames = d_in_ + static_cast<size_t>(k) * S_ * pad_;
+    if (frame_present) {
+        SDX_CUDA(cudaStreamWaitEvent(stream_, h2d_[static_cast<size_t>(k)], 0));
+        if (e.ssf_enabled) {
+            SsfArgs a{};
+            a.frames = frames;
+            a.frame_stride = pad_;
+            a.ref = d_ref_;
+            a.D = D_;
+            a.eta = e.eta;
+            a.max_skip = cfg_.max_skip;
+            a.ctl = dev_.ctl;
+            a.mt_state = mt_;
+            launch_ssf_reduce(a, S_, stream_);
+        }
+        launch_ctl_begin(dev_.ctl, S_, n_, e.guidance_mode, e.ssf_enabled ? kIngestSsf : kIngestAlways, -1, 1,
+                         dev_.rows, dev_.n_rows, dev_.slot_row_c, dev_.slot_row_n, stream_);
+        CommitArgs ca{};
+        ca.frames = frames;
+        ca.frame_stride = pad_;
+        ca.ref = e.ssf_enabled ? d_ref_ : nullptr;
+        ca.D = D_;
+        ca.x0 = dev_.x0;
+        ca.n = n_;
+        ca.d = d_;
+        ca.ctl = dev_.ctl;
+        launch_commit_encode(ca, S_, stream_);
+    } else {
+        launch_ctl_begin(dev_.ctl, S_, n_, e.guidance_mode, kIngestAlways, -1, 0, dev_.rows, dev_.n_rows,
+                         dev_.slot_row_c, dev_.slot_row_n, stream_);
+    }
+    launch_step(dev_.step_args(), S_, stream_);
+    launch_ctl_end(dev_.ctl, S_, n_, e.guidance_mode, dev_.log, frame_present ? 1 : 0, stream_);
+    SDX_CUDA(cudaMemcpyAsync(h_log_ + static_cast<size_t>(k) * S_, dev_.log, sizeof(LogEntry) * S_,
+                             cudaMemcpyDeviceToHost, stream_));
+    if (!resident_ || copy_outputs_)
+        SDX_CUDA(cudaMemcpyAsync(h_out_ + static_cast<size_t>(k) * S_ * out_bytes_, dev_.emitted,
+                                 out_bytes_ * S_, cudaMemcpyDeviceToHost, stream_));
+    SDX_CUDA(cudaEventRecord(done_[static_cast<size_t>(k)], stream_));
+}
+
+void Pipeline::flush_below(StreamHost& h, int64_t limit, std::vector<Out>& staged) {
+    // EngineStage::flush_skips_below (pipeline.cpp:102-116)
+    while (!h.pending_skips.empty() && h.pending_skips.front() < limit) {
+        const int64_t seq = h.pending_skips.front();
+        h.pending_skips.pop_front();
+        if (!h.last_output) {
+            h.stale += 1;
+            continue;
+        }
+        h.duplicates += 1;
+        staged.push_back(Out{seq, h.last_output});
+    }
+}
+
+void Pipeline::process(int k, bool frame_present) {
+    const auto& e = cfg_.engine;
+    const size_t cap8 = static_cast<size_t>(e.queue_capacity) * 8;
+    for (int s = 0; s < S_; ++s) {
+        StreamHost& h = st_[static_cast<size_t>(s)];
+        if (h.incomplete) continue;
+        const LogEntry& L = h_log_[static_cast<size_t>(k) * S_ + s];
+        std::vector<Out> staged;
+        if (frame_present) {
+            h.frames_in += 1;
+            const bool skip = e.ssf_enabled && L.decision == SDX_GATE_SKIP;
+            if (e.ssf_enabled) {
+                h.examined += 1;
+                if (skip) h.skipped += 1;
+                h.decisions.push_back(L.decision);
+            }
+            if (skip) h.pending_skips.push_back(L.seq_in);
+            else h.eng->ingest(L.seq_in);
+        }
+        if (!h.eng->idle()) {
+            const auto t = h.eng->tick();
+            if (t.emitted != (L.emit_seq >= 0) || (t.emitted && t.seq != L.emit_seq)) {
+                h.incomplete = true;
+                h.error = "device/host engine mirror diverged";
+                continue;
+            }
+            if (t.emitted) {
+                if (L.nonfinite) {
+                    h.incomplete = true;
+                    h.error = "tick: non-finite latent at emission";
+                    continue;
+                }
+                flush_below(h, t.seq, staged);
+                auto payload = std::make_shared<std::vector<uint8_t>>(out_bytes_);
+                std::memcpy(payload->data(), h_out_ + (static_cast<size_t>(k) * S_ + s) * out_bytes_, out_bytes_);
+                h.lats.push_back(t.emit_tick - t.ingest_tick);
+                h.last_output = payload;
+                staged.push_back(Out{t.seq, payload});
+            }
+        }
+        flush_below(h, h.eng->min_inflight_seq(), staged);
+        // out_q: bounded drop-oldest (queue.hpp:23-34), drained every iteration
+        size_t first = 0;
+        if (staged.size() > cap8) {
+            first = staged.size() - cap8;
+            h.output_drops += first;
+        }
+        for (size_t i = first; i < staged.size(); ++i) {
+            h.sink.push_back(staged[i]);
+            h.frames_out += 1;
+        }
+    }
+}
+
+void Pipeline::drain_completed(bool block_all) {
+    while (!inflight_.empty()) {
+        const auto [k, fp] = inflight_.front();
+        cudaEvent_t ev = done_[static_cast<size_t>(k)];
+        if (block_all) {
+            SDX_CUDA(cudaEventSynchronize(ev));
+        } else {
+            const cudaError_t q = cudaEventQuery(ev);
+            if (q == cudaErrorNotReady) return;
+            SDX_CUDA(q);
+        }
+        process(k, fp);
+        inflight_.pop_front();
+    }
+}
+
+void Pipeline::push(const uint8_t* frames) {
+    SDX_CUDA(cudaSetDevice(device_));
+    const int k = static_cast<int>(iter_ % K_);
+    while (static_cast<int>(inflight_.size()) >= K_) {
+        const auto [kk, fp] = inflight_.front();
+        SDX_CUDA(cudaEventSynchronize(done_[static_cast<size_t>(kk)]));
+        process(kk, fp);
+        inflight_.pop_front();
+    }
+    if (frames) {
+        const uint8_t* src = frames;
+        cudaPointerAttributes attr{};
+        const bool pinned = cudaPointerGetAttributes(&attr, frames) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (!pinned) {
+            uint8_t* stage = h_in_ + static_cast<size_t>(k) * S_ * D_;
+            std::memcpy(stage, frames, static_cast<size_t>(S_) * D_);
+            src = stage;
+        }
+        if (pad_ == D_) {
+            SDX_CUDA(cudaMemcpyAsync(d_in_ + static_cast<size_t>(k) * S_ * pad_, src, static_cast<size_t>(S_) * D_,
+                                     cudaMemcpyHostToDevice, copy_));
+        } else {
+            SDX_CUDA(cudaMemcpy2DAsync(d_in_ + static_cast<size_t>(k) * S_ * pad_, static_cast<size_t>(pad_), src,
+                                       static_cast<size_t>(D_), static_cast<size_t>(D_), static_cast<size_t>(S_),
+                                       cudaMemcpyHostToDevice, copy_));
+        }
+        SDX_CUDA(cudaEventRecord(h2d_[static_cast<size_t>(k)], copy_));
+    } else {
+        // resident mode: frames already in ring slot k (upload_resident)
+        SDX_CUDA(cudaEventRecord(h2d_[static_cast<size_t>(k)], stream_));
+    }
+    launch_iteration(k, true);
+    inflight_.push_back({k, true});
+    iter_ += 1;
+    drain_completed(false);
+}
+
+void Pipeline::upload_resident(const uint8_t* frames, int count) {
+    // Stage `count` iterations' frames into the device ring (<= K) so timed
+    // pushes run with inputs already in HBM.
+    SDX_CUDA(cudaSetDevice(device_));
+    if (count > K_) raise(SDX_INVALID_ARGUMENT, "upload_resident: count exceeds ring_depth");
+    sync();
+    for (int k = 0; k < count; ++k)
+        SDX_CUDA(cudaMemcpy2D(d_in_ + static_cast<size_t>(k) * S_ * pad_, static_cast<size_t>(pad_),
+                              frames + static_cast<size_t>(k) * S_ * D_, static_cast<size_t>(D_),
+                              static_cast<size_t>(D_), static_cast<size_t>(S_), cudaMemcpyHostToDevice));
+    resident_count_ = count;
+}
+
+void Pipeline::push_resident(bool copy_outputs) {
+    if (resident_count_ < 1) raise(SDX_LOGIC_ERROR, "push_resident: no resident frames uploaded");
+    // ring slot k holds resident frame (iter % resident_count); keep them by
+    // pinning K == resident_count usage
+    resident_ = true;
+    copy_outputs_ = copy_outputs;
+    const int64_t saved = iter_;
+    (void)saved;
+    if (resident_count_ != K_) raise(SDX_LOGIC_ERROR, "push_resident: upload exactly ring_depth frames");
+    push(nullptr);
+    resident_ = false;
+}
+
+void Pipeline::finish() {
+    SDX_CUDA(cudaSetDevice(device_));
+    drain_completed(true);
+    int rem = 0;
+    for (auto& h : st_) {
+        if (h.incomplete || h.eng->idle()) continue;
+        const auto steps = h.eng->step_indices();
+        rem = std::max(rem, n_ - steps.front());
+    }
+    for (int i = 0; i < rem; ++i) {
+        const int k = static_cast<int>(iter_ % K_);
+        while (static_cast<int>(inflight_.size()) >= K_) drain_completed(true);
+        launch_iteration(k, false);
+        inflight_.push_back({k, false});
+        iter_ += 1;
+    }
+    drain_completed(true);
+    for (auto& h : st_) {
+        if (h.incomplete) continue;
+        std::vector<Out> staged;
+        flush_below(h, INT64_MAX, staged);  // EngineStage::finish (pipeline.cpp:84-86)
+        for (auto& o : staged) {
+            h.sink.push_back(o);
+            h.frames_out += 1;
+        }
+    }
+}
+
+bool Pipeline::pop(int stream, int64_t* seq, void* payload) {
+    if (stream < 0 || stream >= S_) raise(SDX_INVALID_ARGUMENT, "pop: stream index out of range");
+    auto& h = st_[static_cast<size_t>(stream)];
+    if (h.sink.empty()) drain_completed(false);
+    if (h.sink.empty()) return false;
+    const Out o = h.sink.front();
+    h.sink.pop_front();
+    *seq = o.seq;
+    if (payload) std::memcpy(payload, o.payload->data(), o.payload->size());
+    return true;
+}
+
+sdx_report Pipeline::report(int stream) const {
+    if (stream < 0 || stream >= S_) raise(SDX_INVALID_ARGUMENT, "report: stream index out of range");
+    const auto& h = st_[static_cast<size_t>(stream)];
+    sdx_report r{};
+    r.frames_in = h.frames_in;
+    r.frames_out = h.frames_out;
+    r.duplicates = h.duplicates;
+    r.stale_skips = h.stale;
+    r.input_drops = 0;
+    r.output_drops = h.output_drops;
+    r.ticks = static_cast<uint64_t>(h.eng->ticks());
+    r.denoiser_calls = h.eng->calls;
+    r.element_evals = h.eng->evals;
+    if (cfg_.engine.ssf_enabled) {
+        r.ssf_examined = h.examined;
+        r.ssf_skipped = h.skipped;
+        r.skip_rate = h.examined == 0 ? 0.0 : static_cast<double>(h.skipped) / static_cast<double>(h.examined);
+    }
+    if (!h.lats.empty()) {
+        int64_t lo = h.lats[0], hi = h.lats[0], sum = 0;
+        for (auto l : h.lats) {
+            lo = std::min(lo, l);
+            hi = std::max(hi, l);
+            sum += l;
+        }
+        r.latency_ticks_min = lo;
+        r.latency_ticks_max = hi;
+        r.latency_ticks_mean = static_cast<double>(sum) / static_cast<double>(h.lats.size());
+    }
+    if (r.frames_out > 0) {
+        r.mean_frame_time_ms = static_cast<double>(r.ticks) / static_cast<double>(r.frames_out);
+        r.throughput_fps = 1000.0 / r.mean_frame_time_ms;
+        r.wall_ms = static_cast<double>(r.ticks);
+    }
+    r.incomplete = h.incomplete ? 1 : 0;
+    return r;
+}
+
+const std::string& Pipeline::error(int stream) const { return st_[static_cast<size_t>(stream)].error; }
+
+void Pipeline::sync() {
+    SDX_CUDA(cudaSetDevice(device_));
+    drain_completed(true);
+    SDX_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void Pipeline::reset_timer() {
+    SDX_CUDA(cudaSetDevice(device_));
+    SDX_CUDA(cudaEventRecord(t0_, stream_));
+}
+
+float Pipeline::device_time_ms() {
+    SDX_CUDA(cudaSetDevice(device_));
+    SDX_CUDA(cudaEventRecord(t1_, stream_));
+    SDX_CUDA(cudaEventSynchronize(t1_));
+    float ms = 0.f;
+    SDX_CUDA(cudaEventElapsedTime(&ms, t0_, t1_));
+    return ms;
+}
+
+}  // namespace sdx

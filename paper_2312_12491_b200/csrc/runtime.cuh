@@ -1,0 +1,197 @@
+// Host runtime of the B200 streaming denoise loop: device-state owners for
+// the engine, the SSF gate and the multi-stream pipeline, plus the host
+// mirror of the reference's engine/pipeline bookkeeping.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <memory>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "device_ctl.cuh"
+#include "kernels_core.cuh"
+
+namespace sdx {
+
+// Host mirror of StreamBatchEngine's frame bookkeeping (engine.cpp:53-211):
+// which frames are in flight at which step.  It never touches latents; the
+// device holds those.  Used for argument validation with the reference's
+// exception semantics and to order the pipeline sink without reading data.
+class EngineMirror {
+  public:
+    struct Frame {
+        int64_t seq;
+        int step;
+        int64_t ingest_tick;
+    };
+    struct TickOut {
+        bool emitted = false;
+        int64_t seq = -1, ingest_tick = 0, emit_tick = 0;
+        uint64_t rows = 0;
+    };
+
+    EngineMirror(int n, int guidance) : n_(n), guidance_(guidance) {}
+
+    void check_ingest(int64_t seq) const;
+    void ingest(int64_t seq);
+    TickOut tick();
+    bool idle() const { return inflight_.empty(); }
+    int64_t ticks() const { return ticks_; }
+    int inflight() const { return static_cast<int>(inflight_.size()); }
+    std::vector<int> step_indices() const;
+    int64_t min_inflight_seq() const;  // INT64_MAX when idle
+    uint64_t calls = 0, evals = 0;
+    bool pending_ingest() const { return pending_; }
+    int64_t pending_seq() const { return pending_seq_; }
+
+  private:
+    int n_, guidance_;
+    std::vector<Frame> inflight_;
+    int64_t ticks_ = 0, last_seq_ = -1;
+    bool pending_ = false;
+    int64_t pending_seq_ = -1;
+};
+
+// Device-resident state of S streams sharing one batched denoiser call.
+struct DeviceEngine {
+    int S = 0, n = 0;
+    long long d = 0;
+    int guidance = 0;
+    double gamma = 1.4, delta = 1.0;
+    bool per_slot_cond = false;
+    StepScalars* tbl = nullptr;
+    float *x_cur = nullptr, *x0 = nullptr, *x0ref = nullptr, *eps_cached = nullptr;
+    float *cond = nullptr, *neg = nullptr, *emitted = nullptr;
+    StreamCtl* ctl = nullptr;
+    RowDesc* rows = nullptr;
+    int* n_rows = nullptr;
+    int *slot_row_c = nullptr, *slot_row_n = nullptr;
+    LogEntry* log = nullptr;  // [S]
+
+    void init(int S_, int n_, long long d_, int guidance_, double gamma_, double delta_,
+              const std::vector<StepScalars>& table, bool per_slot_cond_);
+    void release();
+    StepArgs step_args() const;
+};
+
+std::vector<StepScalars> make_step_table(const sdx_step* steps, int n, int lcm_mode, double data_variance);
+
+class Engine {
+  public:
+    Engine(const sdx_config& cfg, const sdx_step* steps, int n, const double* eps_cached,
+           const double* neg, int device);
+    ~Engine();
+    void ingest(int64_t seq, const double* x0, const double* cond);
+    sdx_tick_result tick(double* x0_hat);
+    EngineMirror& mirror() { return mirror_; }
+    float last_tick_ms() const { return last_ms_; }
+    void reset_counters() { mirror_.calls = 0; mirror_.evals = 0; }
+
+  private:
+    sdx_config cfg_;
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    cudaEvent_t ev0_ = nullptr, ev1_ = nullptr;
+    DeviceEngine dev_;
+    EngineMirror mirror_;
+    float* h_stage_ = nullptr;  // pinned, 2 x d floats
+    LogEntry* h_log_ = nullptr;
+    std::vector<std::vector<float>> slot_cond_;  // last condition uploaded per slot
+    float last_ms_ = 0.f;
+    bool timed_ = false;
+};
+
+class Ssf {
+  public:
+    Ssf(double eta, uint64_t seed, int max_skip, int64_t frame_bytes, int device);
+    ~Ssf();
+    void gate(const uint8_t* frames, int nframes, int* decisions, double* sims);
+    uint64_t examined() const { return examined_; }
+    uint64_t skipped() const { return skipped_; }
+
+  private:
+    double eta_;
+    int max_skip_;
+    int64_t D_;
+    int device_;
+    cudaStream_t stream_ = nullptr;
+    uint8_t *d_frames_ = nullptr, *d_ref_ = nullptr;
+    StreamCtl* ctl_ = nullptr;
+    unsigned long long* mt_ = nullptr;
+    int* dec_ = nullptr;
+    double* sims_ = nullptr;
+    int batch_ = 0;
+    uint64_t examined_ = 0, skipped_ = 0;
+};
+
+// Initial MT19937-64 state words for seed (std::mt19937_64 seeding).
+void mt_seed_words(uint64_t seed, unsigned long long* out312);
+
+class Pipeline {
+  public:
+    Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const double* eps_cached,
+             const double* cond, const double* neg, int device);
+    ~Pipeline();
+    void push(const uint8_t* frames);
+    void upload_resident(const uint8_t* frames, int count);
+    void push_resident(bool copy_outputs);
+    void finish();
+    const std::string& error(int stream) const;
+    bool pop(int stream, int64_t* seq, void* payload);
+    sdx_report report(int stream) const;
+    const std::vector<int>& decisions(int stream) const { return st_[stream].decisions; }
+    void sync();
+    void reset_timer();
+    float device_time_ms();
+
+  private:
+    struct Out {
+        int64_t seq;
+        std::shared_ptr<std::vector<uint8_t>> payload;
+    };
+    struct StreamHost {
+        std::unique_ptr<EngineMirror> eng;
+        std::deque<int64_t> pending_skips;
+        std::shared_ptr<std::vector<uint8_t>> last_output;
+        std::deque<Out> sink;
+        std::vector<int64_t> lats;
+        std::vector<int> decisions;
+        uint64_t frames_in = 0, frames_out = 0, duplicates = 0, stale = 0, output_drops = 0;
+        uint64_t examined = 0, skipped = 0;
+        bool incomplete = false;
+        std::string error;
+    };
+    void launch_iteration(int k, bool frame_present);
+    void process(int k, bool frame_present);
+    void drain_completed(bool block_all);
+    void flush_below(StreamHost& h, int64_t limit, std::vector<Out>& staged);
+
+    sdx_pipeline_config cfg_;
+    int S_, n_, K_;
+    int64_t D_;
+    long long d_;
+    size_t out_bytes_;
+    int device_;
+    cudaStream_t stream_ = nullptr, copy_ = nullptr;
+    DeviceEngine dev_;
+    int64_t pad_ = 0;
+    bool resident_ = false, copy_outputs_ = true;
+    int resident_count_ = 0;
+    std::vector<cudaEvent_t> h2d_;
+    uint8_t *d_in_ = nullptr, *d_ref_ = nullptr;
+    unsigned long long* mt_ = nullptr;
+    uint8_t *h_in_ = nullptr, *h_out_ = nullptr;
+    LogEntry* h_log_ = nullptr;
+    std::vector<cudaEvent_t> done_;
+    std::deque<std::pair<int, bool>> inflight_;  // (ring slot, frame_present)
+    int64_t iter_ = 0;
+    std::vector<StreamHost> st_;
+    cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+};
+
+}  // namespace sdx

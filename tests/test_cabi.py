@@ -1,0 +1,81 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every
+symbol include/stagger_b200.h declares, the host precompute matches the oracle
+bit-for-bit, and argument validation follows the reference's error contract
+(validation runs before any CUDA call)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "stagger_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(sdx_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2312_12491_b200 import _lib
+
+    names = declared_symbols()
+    assert len(names) > 30
+    for n in names:
+        assert hasattr(_lib.lib, n), n
+    assert set(names) == set(_lib.EXPORTED)
+    assert _lib.lib.sdx_abi_version() == 1
+
+
+def test_host_precompute_bitwise_vs_oracle(sg, orc):
+    for n, entry in [(1, 1.0), (4, 1.0), (10, 0.5), (50, 1.0)]:
+        got = sg.build_schedule(n, 1000, entry)
+        taus, a, b = orc.schedule(n, 1000, entry)
+        assert [s.tau for s in got] == taus
+        assert np.array_equal([s.alpha for s in got], a) and np.array_equal([s.beta for s in got], b)
+    assert sg.derive_seed(0, 2) == orc.derive_seed(0, 2)
+    assert np.array_equal(sg.sample_gaussian(1234, 1001), orc.gaussian(1234, 1001))
+    cfg = sg.EngineConfig(n_steps=4, d_latent=33, seed=9)
+    pc = sg.build_precompute(cfg)
+    e = orc.engine(__import__("oracle.oracle", fromlist=["make_cfg"]).make_cfg(n_steps=4, d_latent=33, seed=9),
+                   np.zeros(33))
+    for i in range(4):
+        assert np.array_equal(pc.eps_cached[i], e.eps_cached(i))
+
+
+def test_schedule_errors(sg):
+    for args in [(1001, 1000, 1.0), (0, 1000, 1.0), (4, 1000, 0.0), (10, 1000, 0.001)]:
+        with pytest.raises(sg.InvalidArgument):
+            sg.build_schedule(*args)
+
+
+def test_config_validation_reports_every_violation(sg):
+    # validate_config collects all violations into one message (core.cpp:26-69)
+    cfg = sg.EngineConfig(n_steps=0, eta=1.0, delta=2.0, d_latent=8)
+    with pytest.raises(sg.InvalidArgument) as ei:
+        sg.StreamBatchEngine(cfg, sg.PrecomputeCache([], np.zeros((0, 8))))
+    msg = str(ei.value)
+    for frag in ("n_steps must be >= 1", "eta out of range", "delta must lie in [0,1]"):
+        assert frag in msg
+
+
+def test_negative_condition_required(sg):
+    cfg = sg.EngineConfig(n_steps=2, guidance_mode="cfg", d_latent=8)
+    with pytest.raises(sg.InvalidArgument):
+        sg.StreamBatchEngine(cfg)
+
+
+def test_cross_frame_attention_unsupported(sg):
+    cfg = sg.EngineConfig(n_steps=2, cross_frame_attention=True, d_latent=8)
+    with pytest.raises(sg.Unsupported):
+        sg.StreamBatchEngine(cfg)
+
+
+def test_null_handles_are_rejected():
+    from paper_2312_12491_b200 import _lib
+
+    r = _lib.sdx_tick_result()
+    assert _lib.lib.sdx_engine_tick(None, C.byref(r), None) == _lib.SDX_INVALID_ARGUMENT
+    assert b"null argument" in _lib.lib.sdx_last_error()

@@ -1,0 +1,133 @@
+"""GPU parity of the device-decided pipeline (sdx_pipeline_*) against the
+oracle's deterministic run_pipeline (pipeline.cpp:152-214): sink order and
+duplicate placement bit-exact, SSF decisions bit-exact, report counters
+identical, payloads within 1e-3 (fp32 latents).  Mirrors test_runtime.cpp."""
+import numpy as np
+import pytest
+
+from oracle.oracle import make_cfg
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+INT_KEYS = ["frames_in", "frames_out", "duplicates", "stale_skips", "input_drops", "output_drops", "ticks",
+            "denoiser_calls", "element_evals", "ssf_examined", "ssf_skipped", "latency_ticks_min",
+            "latency_ticks_max"]
+
+
+def u8_stream(kind, D, seed, n):
+    rng = np.random.default_rng(seed)
+    base = rng.integers(0, 256, D, dtype=np.uint8)
+    out = []
+    for i in range(n):
+        if kind == "static":
+            f = base
+        elif kind == "dynamic":
+            f = rng.integers(0, 256, D, dtype=np.uint8)
+        else:  # near-static with cuts: sims straddle 0.98
+            if i % 23 == 22:
+                base = rng.integers(0, 256, D, dtype=np.uint8)
+            f = base.copy()
+            k = int(rng.integers(0, D // 30))
+            idx = rng.integers(0, D, k)
+            f[idx] = rng.integers(0, 256, k, dtype=np.uint8)
+        out.append(f)
+    return np.stack(out)
+
+
+def compare(sg, orc, frames, n, mode="none", ssf=True, seed=3, max_skip=0, lcm="exact"):
+    D = frames.shape[1]
+    neg = orc.gaussian(orc.derive_seed(seed, 5), D) if mode in ("cfg", "onetime_negative") else None
+    ocfg = make_cfg(n_steps=n, guidance_mode=mode, ssf_enabled=ssf, seed=seed, d_latent=D, lcm_mode=lcm)
+    want = orc.run_pipeline(ocfg, frames.astype(np.float64), neg=neg, max_skip=max_skip)
+    cfg = sg.EngineConfig(n_steps=n, guidance_mode=mode, ssf_enabled=ssf, seed=seed, d_latent=D,
+                          negative_condition=neg, lcm_mode=lcm)
+    sink, rep = sg.run_pipeline(cfg, frames, max_skip=max_skip)
+    assert [s for s, _ in sink] == want.seq.tolist()
+    worst = max((float(np.max(np.abs(p.astype(np.float64) - w))) for (_, p), w in zip(sink, want.payload)),
+                default=0.0)
+    assert worst <= TOL, worst
+    for k in INT_KEYS:
+        assert rep[k] == want.report[k], (k, rep[k], want.report[k])
+    assert rep["incomplete"] is False
+    for k in ("skip_rate", "latency_ticks_mean", "mean_frame_time_ms", "throughput_fps", "wall_ms"):
+        assert rep[k] == pytest.approx(want.report[k], rel=1e-12)
+    return want, sink, rep
+
+
+@pytest.mark.parametrize("kind", ["static", "dynamic", "periodic"])
+@pytest.mark.parametrize("n", [1, 4])
+def test_pipeline_matches_oracle(sg, orc, kind, n):
+    frames = u8_stream(kind, 1024, 10 + n, 120)
+    compare(sg, orc, frames, n)
+
+
+@pytest.mark.parametrize("mode", ["none", "cfg", "self_negative", "onetime_negative"])
+def test_pipeline_modes(sg, orc, mode):
+    frames = u8_stream("periodic", 2048, 4, 80)
+    compare(sg, orc, frames, 3, mode=mode)
+
+
+def test_pipeline_static_scene_duplicates(sg, orc):
+    # test_runtime.cpp:169-188 shape: one processed frame, duplicates for the rest
+    frames = u8_stream("static", 512, 1, 20)
+    want, sink, rep = compare(sg, orc, frames, 4)
+    assert rep["ssf_skipped"] == 19 and rep["duplicates"] == 19 and rep["element_evals"] == 4
+
+
+def test_pipeline_ssf_off_equals_on_for_dynamic(sg, orc):
+    # test_runtime.cpp:190-211
+    frames = u8_stream("dynamic", 1024, 2, 60)
+    _, a, _ = compare(sg, orc, frames, 3, ssf=False)
+    _, b, rep = compare(sg, orc, frames, 3, ssf=True)
+    assert rep["ssf_skipped"] == 0
+    assert [s for s, _ in a] == [s for s, _ in b]
+    for (_, x), (_, y) in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_pipeline_max_skip(sg, orc):
+    frames = u8_stream("static", 4096, 3, 60)
+    want, _, rep = compare(sg, orc, frames, 2, max_skip=10)
+    assert rep["ssf_skipped"] < 59
+
+
+def test_pipeline_latent_16384(sg, orc):
+    # the 4x64x64 latent size, near-static stream
+    frames = u8_stream("periodic", 16384, 5, 40)
+    compare(sg, orc, frames, 4, mode="self_negative")
+
+
+def test_multistream_equals_independent_streams(sg, orc):
+    # cfg4 shape: S streams batched into one tick == S independent runs with seed base+s
+    S, D, n, N = 8, 1024, 1, 50
+    streams = [u8_stream("periodic", D, 100 + s, N) for s in range(S)]
+    cfg = sg.EngineConfig(n_steps=n, guidance_mode="self_negative", ssf_enabled=True, seed=40, d_latent=D)
+    p = sg.Pipeline(cfg, S, D)
+    sinks = [[] for _ in range(S)]
+    for i in range(N):
+        p.push(np.stack([streams[s][i] for s in range(S)]))
+        for s in range(S):
+            sinks[s].extend(p.pop_all(s))
+    p.finish()
+    for s in range(S):
+        sinks[s].extend(p.pop_all(s))
+        want = orc.run_pipeline(make_cfg(n_steps=n, guidance_mode="self_negative", ssf_enabled=True, seed=40 + s,
+                                         d_latent=D), streams[s].astype(np.float64))
+        assert [q for q, _ in sinks[s]] == want.seq.tolist()
+        assert p.decisions(s).tolist() == want.decisions.tolist()
+        for (_, x), w in zip(sinks[s], want.payload):
+            assert np.max(np.abs(x - w)) <= TOL
+        rep = p.report(s)
+        for k in INT_KEYS:
+            assert rep[k] == want.report[k], (s, k)
+    p.close()
+
+
+def test_pipeline_failure_marks_incomplete(sg):
+    # test_runtime.cpp:303-316 analogue: a frame of the wrong width is rejected
+    cfg = sg.EngineConfig(n_steps=2, d_latent=8)
+    p = sg.Pipeline(cfg, 1, 8)
+    p.push(np.ones(8, dtype=np.uint8))
+    with pytest.raises(sg.InvalidArgument):
+        p.push(np.ones(3, dtype=np.uint8))
+    p.close()
