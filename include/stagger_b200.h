@@ -188,6 +188,13 @@ const char* sdx_pipeline_error_message(sdx_pipeline* p, int stream);
  * call reading them in place (no H2D; output D2H only when copy_outputs). */
 int sdx_pipeline_upload_resident(sdx_pipeline* p, const uint8_t* frames, int count);
 int sdx_pipeline_push_resident(sdx_pipeline* p, int copy_outputs);
+/* Per-kernel timing with CUDA events on the pipeline stream (resets the
+ * accumulators); kernel_times returns the summed device ms and launch counts of
+ * the SSF reduction and of the fused step kernel since set_profile(1), and the
+ * number of library kernel launches issued. */
+int sdx_pipeline_set_profile(sdx_pipeline* p, int on);
+int sdx_pipeline_kernel_times(sdx_pipeline* p, double* ssf_ms, int64_t* ssf_launches, double* step_ms,
+                              int64_t* step_launches, int64_t* total_launches);
 int sdx_pipeline_device_time_ms(sdx_pipeline* p, float* ms); /* since last reset */
 int sdx_pipeline_reset_timer(sdx_pipeline* p);
 

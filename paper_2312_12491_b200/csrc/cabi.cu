@@ -255,6 +255,27 @@ int sdx_pipeline_push_resident(sdx_pipeline* p, int copy_outputs) {
     });
 }
 
+int sdx_pipeline_set_profile(sdx_pipeline* p, int on) {
+    return guarded([&] {
+        NEED(p);
+        p->impl.set_profile(on != 0);
+    });
+}
+int sdx_pipeline_kernel_times(sdx_pipeline* p, double* ssf_ms, int64_t* ssf_launches, double* step_ms,
+                              int64_t* step_launches, int64_t* total_launches) {
+    return guarded([&] {
+        NEED(p);
+        double a = 0, b = 0;
+        long long na = 0, nb = 0;
+        p->impl.kernel_times(&a, &na, &b, &nb);
+        if (ssf_ms) *ssf_ms = a;
+        if (ssf_launches) *ssf_launches = na;
+        if (step_ms) *step_ms = b;
+        if (step_launches) *step_launches = nb;
+        if (total_launches) *total_launches = p->impl.launches();
+    });
+}
+
 // ---- pinned host memory ----
 int sdx_host_alloc(size_t bytes, void** out) {
     return guarded([&] {

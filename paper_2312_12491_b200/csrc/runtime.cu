@@ -490,6 +490,7 @@ Pipeline::~Pipeline() {
     if (h_log_) cudaFreeHost(h_log_);
     for (auto ev : done_) cudaEventDestroy(ev);
     for (auto ev : h2d_) cudaEventDestroy(ev);
+    for (auto ev : kt_) cudaEventDestroy(ev);
     if (t0_) cudaEventDestroy(t0_);
     if (t1_) cudaEventDestroy(t1_);
     if (stream_) cudaStreamDestroy(stream_);
@@ -511,7 +512,9 @@ void Pipeline::launch_iteration(int k, bool frame_present) {
             a.max_skip = cfg_.max_skip;
             a.ctl = dev_.ctl;
             a.mt_state = mt_;
+            if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 0], stream_));
             launch_ssf_reduce(a, S_, stream_);
+            if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 1], stream_));
         }
         launch_ctl_begin(dev_.ctl, S_, n_, e.guidance_mode, e.ssf_enabled ? kIngestSsf : kIngestAlways, -1, 1,
                          dev_.rows, dev_.n_rows, dev_.slot_row_c, dev_.slot_row_n, stream_);
@@ -529,7 +532,10 @@ void Pipeline::launch_iteration(int k, bool frame_present) {
         launch_ctl_begin(dev_.ctl, S_, n_, e.guidance_mode, kIngestAlways, -1, 0, dev_.rows, dev_.n_rows,
                          dev_.slot_row_c, dev_.slot_row_n, stream_);
     }
+    if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 2], stream_));
     launch_step(dev_.step_args(), S_, stream_);
+    if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 3], stream_));
+    launches_ += frame_present ? (cfg_.engine.ssf_enabled ? 5 : 4) : 3;
     launch_ctl_end(dev_.ctl, S_, n_, e.guidance_mode, dev_.log, frame_present ? 1 : 0, stream_);
     SDX_CUDA(cudaMemcpyAsync(h_log_ + static_cast<size_t>(k) * S_, dev_.log, sizeof(LogEntry) * S_,
                              cudaMemcpyDeviceToHost, stream_));
@@ -555,6 +561,17 @@ void Pipeline::flush_below(StreamHost& h, int64_t limit, std::vector<Out>& stage
 
 void Pipeline::process(int k, bool frame_present) {
     const auto& e = cfg_.engine;
+    if (profile_) {
+        float ms = 0.f;
+        if (frame_present && e.ssf_enabled) {
+            SDX_CUDA(cudaEventElapsedTime(&ms, kt_[static_cast<size_t>(k) * 4 + 0], kt_[static_cast<size_t>(k) * 4 + 1]));
+            ktime_[0] += ms;
+            kcount_[0] += 1;
+        }
+        SDX_CUDA(cudaEventElapsedTime(&ms, kt_[static_cast<size_t>(k) * 4 + 2], kt_[static_cast<size_t>(k) * 4 + 3]));
+        ktime_[1] += ms;
+        kcount_[1] += 1;
+    }
     const size_t cap8 = static_cast<size_t>(e.queue_capacity) * 8;
     for (int s = 0; s < S_; ++s) {
         StreamHost& h = st_[static_cast<size_t>(s)];
@@ -776,6 +793,26 @@ void Pipeline::sync() {
 void Pipeline::reset_timer() {
     SDX_CUDA(cudaSetDevice(device_));
     SDX_CUDA(cudaEventRecord(t0_, stream_));
+}
+
+void Pipeline::set_profile(bool on) {
+    SDX_CUDA(cudaSetDevice(device_));
+    sync();
+    if (on && kt_.empty()) {
+        kt_.resize(static_cast<size_t>(K_) * 4);
+        for (auto& ev : kt_) SDX_CUDA(cudaEventCreate(&ev));
+    }
+    profile_ = on;
+    ktime_[0] = ktime_[1] = 0.0;
+    kcount_[0] = kcount_[1] = 0;
+    launches_ = 0;
+}
+
+void Pipeline::kernel_times(double* ssf_ms, long long* ssf_n, double* step_ms, long long* step_n) const {
+    *ssf_ms = ktime_[0];
+    *ssf_n = kcount_[0];
+    *step_ms = ktime_[1];
+    *step_n = kcount_[1];
 }
 
 float Pipeline::device_time_ms() {

@@ -148,6 +148,11 @@ class Pipeline {
     void sync();
     void reset_timer();
     float device_time_ms();
+    // Per-kernel device time (CUDA events around the SSF reduction and the
+    // step kernel, on the launching stream), accumulated while profiling.
+    void set_profile(bool on);
+    void kernel_times(double* ssf_ms, long long* ssf_n, double* step_ms, long long* step_n) const;
+    long long launches() const { return launches_; }
 
   private:
     struct Out {
@@ -192,6 +197,11 @@ class Pipeline {
     int64_t iter_ = 0;
     std::vector<StreamHost> st_;
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;
+    bool profile_ = false;
+    std::vector<cudaEvent_t> kt_;  // [K][4]
+    double ktime_[2] = {0, 0};
+    long long kcount_[2] = {0, 0};
+    long long launches_ = 0;
 };
 
 }  // namespace sdx

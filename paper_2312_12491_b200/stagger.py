@@ -413,6 +413,17 @@ class Pipeline:
     def reset_timer(self):
         _check(L.lib.sdx_pipeline_reset_timer(self._h))
 
+    def set_profile(self, on: bool = True):
+        _check(L.lib.sdx_pipeline_set_profile(self._h, int(on)))
+
+    def kernel_times(self) -> dict:
+        a, b = C.c_double(), C.c_double()
+        na, nb, nt = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(L.lib.sdx_pipeline_kernel_times(self._h, C.byref(a), C.byref(na), C.byref(b), C.byref(nb),
+                                               C.byref(nt)))
+        return dict(ssf_ms=a.value, ssf_launches=na.value, step_ms=b.value, step_launches=nb.value,
+                    launches=nt.value)
+
     def device_time_ms(self) -> float:
         v = C.c_float()
         _check(L.lib.sdx_pipeline_device_time_ms(self._h, C.byref(v)))

@@ -131,11 +131,22 @@ def test_error_contract(sg, orc):
 
 
 def test_nonfinite_emission_raises(sg, orc):
-    # engine.cpp:166-168: non-finite latent at emission -> runtime_error
+    # engine.cpp:166-168: non-finite latent at emission -> runtime_error.  gamma = inf
+    # passes validate_config (gamma >= 0) and makes the CFG combine non-finite in both
+    # the fp64 reference and the device path.
+    from oracle.oracle import OracleError
+
     d = 8
-    cfg = sg.EngineConfig(n_steps=1, d_latent=d)
+    neg = np.linspace(-1, 1, d)
+    ocfg = make_cfg(n_steps=1, guidance_mode="cfg", gamma=float("inf"), d_latent=d)
+    eo = orc.engine(ocfg, np.zeros(d), neg)
+    eo.ingest(0, np.ones(d))
+    with pytest.raises(OracleError) as ei:
+        eo.tick()
+    assert ei.value.code == 3
+    cfg = sg.EngineConfig(n_steps=1, guidance_mode="cfg", gamma=float("inf"), d_latent=d, negative_condition=neg)
     ed = sg.StreamBatchEngine(cfg)
-    ed.ingest(0, np.full(d, 1e38), np.full(d, -1e38))
+    ed.ingest(0, np.ones(d), np.zeros(d))
     with pytest.raises(sg.StaggerRuntimeError):
         ed.tick()
 
