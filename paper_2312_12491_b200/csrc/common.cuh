@@ -54,6 +54,8 @@ struct StepScalars {
     double alpha;
     int tau;
     int pad;
+    // fp32 copies for the device step (inverses precomputed in fp64)
+    float f_sa, f_sb, f_isa, f_isb, f_cs, f_co, f_an, f_beta;
 };
 
 }  // namespace sdx

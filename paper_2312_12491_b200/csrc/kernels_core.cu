@@ -126,130 +126,6 @@ __global__ void ctl_begin_kernel(StreamCtl* __restrict__ ctl, int S, int n, int 
 }
 
 // ---------------------------------------------------------------------------
-// fused step
-// ---------------------------------------------------------------------------
-
-struct ElemIn {
-    double x;        // current latent (or formed x_tau0)
-    double mu, neg;  // condition / negative means (analytic)
-    double x0;       // input latent (self-negative reference)
-    double x0ref;    // stored onetime reference
-    double renoise;  // eps_cached[step+1]
-    double ec, en;   // external eps rows (UNet) when ext
-};
-
-// Returns the new latent (x_{next}) or x0_hat at the terminal step; writes the
-// freshly initialised onetime reference into *x0ref_out when init_now.
-template <bool kExt>
-__device__ __forceinline__ double step_elem(const ElemIn& in, const StepScalars& st,
-                                            const StepScalars& st0, const StepScalars& nx,
-                                            int guidance, double gamma, double delta,
-                                            bool init_now, bool terminal, double* x0ref_out) {
-    const double x = in.x;
-    // denoiser rows (AnalyticGaussianModel::do_predict: scale*(x - sa*mu))
-    const double ec = kExt ? in.ec : st.an_scale * (x - st.sa * in.mu);
-    double eps = ec;
-    if (guidance == SDX_GUIDANCE_CFG) {
-        const double en = kExt ? in.en : st.an_scale * (x - st.sa * in.neg);
-        eps = en + gamma * (ec - en);  // cfg_combine(neg, cond, gamma)
-    } else if (guidance == SDX_GUIDANCE_SELF_NEGATIVE || guidance == SDX_GUIDANCE_ONETIME_NEGATIVE) {
-        double xr;
-        if (guidance == SDX_GUIDANCE_SELF_NEGATIVE) {
-            xr = in.x0;
-        } else if (init_now) {
-            // init row: predict_x0(x_tau0, steps[0], eps_neg)
-            const double en = kExt ? in.en : st0.an_scale * (x - st0.sa * in.neg);
-            xr = (x - st0.sb * en) / st0.sa;
-            *x0ref_out = xr;
-        } else {
-            xr = in.x0ref;
-        }
-        if (st.beta > 0.0) {
-            const double ev = (x - st.sa * xr) / st.sb;  // virtual_residual_noise
-            const double dv = delta * ev;                // rcfg_combine
-            eps = dv + gamma * (ec - dv);
-        }
-    }
-    // consistency_step: x0_hat = c_skip*x + c_out*predict_x0(x, eps)
-    const double px0 = (x - st.sb * eps) / st.sa;
-    const double xh = st.c_skip * x + st.c_out * px0;
-    if (terminal) return xh;
-    return nx.sa * xh + nx.sb * in.renoise;  // forward_diffuse(x0_hat, next, eps_cached[next])
-}
-
-template <bool kExt, int kVec>
-__global__ void __launch_bounds__(256) step_kernel(StepArgs a) {
-    const int s = blockIdx.z;
-    const int slot = blockIdx.y;
-    const StreamCtl& c = a.ctl[s];
-    if (!c.tick_now) return;
-    const SlotCtl sc = c.slot[slot];
-    if (sc.seq < 0) return;
-    const int step = static_cast<int>(c.ticks - sc.ingest_tick);
-    const bool terminal = step + 1 >= a.n;
-    const bool entering = sc.entering != 0;
-    const bool init_now = a.guidance == SDX_GUIDANCE_ONETIME_NEGATIVE && sc.init == 0;
-    const StepScalars st = a.tbl[step];
-    const StepScalars st0 = a.tbl[0];
-    const StepScalars nx = a.tbl[terminal ? a.n : step + 1];
-
-    const long long sd = static_cast<long long>(s) * a.n + slot;  // (stream, slot) row
-    const long long d = a.d;
-    const float* __restrict__ x0 = a.x0 + sd * d;
-    float* __restrict__ xcur = a.x_cur + sd * d;
-    float* __restrict__ x0ref = a.x0ref ? a.x0ref + sd * d : nullptr;
-    const float* __restrict__ e0 = a.eps_cached + (static_cast<long long>(s) * a.n) * d;
-    const float* __restrict__ en_ = terminal ? nullptr
-                                             : a.eps_cached + (static_cast<long long>(s) * a.n + step + 1) * d;
-    const float* __restrict__ mu = a.cond + s * a.cond_stream_stride + slot * a.cond_slot_stride;
-    const float* __restrict__ ng = a.neg ? a.neg + static_cast<long long>(s) * d : nullptr;
-    float* __restrict__ out = terminal ? a.emitted + static_cast<long long>(s) * d : xcur;
-    const float* __restrict__ ecr = nullptr;
-    const float* __restrict__ enr = nullptr;
-    if (kExt) {
-        ecr = a.eps_ext + static_cast<long long>(a.slot_row_c[s * kMaxSteps + slot]) * a.eps_ext_stride;
-        const int rn = a.slot_row_n[s * kMaxSteps + slot];
-        enr = rn >= 0 ? a.eps_ext + static_cast<long long>(rn) * a.eps_ext_stride : nullptr;
-    }
-
-    int bad = 0;
-    const long long stride = static_cast<long long>(gridDim.x) * blockDim.x * kVec;
-    for (long long i = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) * kVec; i < d;
-         i += stride) {
-#pragma unroll
-        for (int v = 0; v < kVec; ++v) {
-            const long long k = i + v;
-            if (kVec > 1 || k < d) {
-                ElemIn in;
-                in.x = entering ? st0.sa * static_cast<double>(x0[k]) + st0.sb * static_cast<double>(e0[k])
-                                : static_cast<double>(xcur[k]);
-                in.mu = kExt ? 0.0 : static_cast<double>(mu[k]);
-                in.neg = (!kExt && ng) ? static_cast<double>(ng[k]) : 0.0;
-                in.x0 = a.guidance == SDX_GUIDANCE_SELF_NEGATIVE ? static_cast<double>(x0[k]) : 0.0;
-                in.x0ref = (a.guidance == SDX_GUIDANCE_ONETIME_NEGATIVE && !init_now)
-                               ? static_cast<double>(x0ref[k]) : 0.0;
-                in.renoise = terminal ? 0.0 : static_cast<double>(en_[k]);
-                if (kExt) {
-                    in.ec = static_cast<double>(ecr[k]);
-                    in.en = enr ? static_cast<double>(enr[k]) : 0.0;
-                }
-                double xr = 0.0;
-                const double y = step_elem<kExt>(in, st, st0, nx, a.guidance, a.gamma, a.delta, init_now,
-                                                 terminal, &xr);
-                if (init_now) x0ref[k] = static_cast<float>(xr);
-                const float yf = static_cast<float>(y);
-                if (terminal && !isfinite(yf)) bad = 1;
-                out[k] = yf;
-            }
-        }
-    }
-    if (terminal) {
-        bad = __syncthreads_or(bad);
-        if (bad && threadIdx.x == 0) atomicOr(&a.ctl[s].nonfinite, 1);
-    }
-}
-
-// ---------------------------------------------------------------------------
 // control: end of an iteration
 // ---------------------------------------------------------------------------
 
@@ -520,24 +396,6 @@ void launch_ctl_begin(StreamCtl* ctl, int S, int n, int guidance, int ingest_mod
     while (threads < S) threads <<= 1;
     ctl_begin_kernel<<<1, threads, 0, st>>>(ctl, S, n, guidance, ingest_mode, host_seq, frame_present, rows,
                                             n_rows, slot_row_c, slot_row_n);
-    SDX_LAUNCH_CHECK();
-}
-
-void launch_step(const StepArgs& a, int S, cudaStream_t st) {
-    const int threads = 256;
-    const bool vec = (a.d % 4) == 0;
-    const long long per_block = threads * (vec ? 4 : 1);
-    long long blocks = (a.d + per_block - 1) / per_block;
-    if (blocks < 1) blocks = 1;
-    if (blocks > 65535) blocks = 65535;
-    dim3 grid(static_cast<unsigned>(blocks), a.n, S);
-    if (a.eps_ext) {
-        if (vec) step_kernel<true, 4><<<grid, threads, 0, st>>>(a);
-        else step_kernel<true, 1><<<grid, threads, 0, st>>>(a);
-    } else {
-        if (vec) step_kernel<false, 4><<<grid, threads, 0, st>>>(a);
-        else step_kernel<false, 1><<<grid, threads, 0, st>>>(a);
-    }
     SDX_LAUNCH_CHECK();
 }
 

@@ -175,6 +175,8 @@ class Pipeline {
     void process(int k, bool frame_present);
     void drain_completed(bool block_all);
     void flush_below(StreamHost& h, int64_t limit, std::vector<Out>& staged);
+    std::shared_ptr<std::vector<uint8_t>> acquire_buffer();
+    std::vector<std::shared_ptr<std::vector<uint8_t>>> pool_;
 
     sdx_pipeline_config cfg_;
     int S_, n_, K_;
