@@ -1,0 +1,36 @@
+/* stagger_b200 kernel-level entry points.
+ *
+ * The building blocks of the batched UNet / TAESD denoiser behind
+ * DenoiserBackend::predict_eps_batch (denoiser.hpp:21-39), exposed on device
+ * pointers so the numerics tests can check each sm_100a kernel against a
+ * PyTorch fp32 reference of the same op.  `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  Tensors are bf16 unless stated; layouts NHWC /
+ * row-major.  Return SDX_* status codes (stagger_b200.h).
+ */
+#ifndef STAGGER_B200_KERNELS_H
+#define STAGGER_B200_KERNELS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* C[M,N] = act(A[M,K] . B[N,K]^T * scale + bias) + residual ; tcgen05 + TMA.
+ * act: 0 none, 1 SiLU, 2 ReLU, 3 GELU(erf).  out_f32: C is fp32 else bf16. */
+int sdx_kernel_gemm(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int M, int N, int K,
+                    const float* bias, const void* residual, int act, int out_f32, float scale, void* stream);
+/* A = [A1 | A2] concatenated along K at column K1. */
+int sdx_kernel_gemm_concat(const void* A1, int64_t lda1, int K1, const void* A2, int64_t lda2, const void* B,
+                           int64_t ldb, void* C, int M, int N, int K, const float* bias, int act, int out_f32,
+                           void* stream);
+/* 3x3 conv, pad 1, stride 1|2, NHWC, w [Cout][3][3][Cin]; implicit GEMM via 4-D TMA.
+ * bias_img: optional [imgs][Cout] per-image bias (time embedding). */
+int sdx_kernel_conv3x3(const void* x, int imgs, int H, int W, int Cin, const void* w, int Cout, int stride,
+                       const float* bias, const float* bias_img, const void* residual, int act, void* out,
+                       int out_f32, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

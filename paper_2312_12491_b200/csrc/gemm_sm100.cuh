@@ -1,0 +1,63 @@
+// tcgen05 / TMA GEMM and implicit-GEMM 3x3 convolution for sm_100a.
+//
+//   C[M, N] = act( A[M, K] . B[N, K]^T * scale + bias[N] + bias_img[m / rows_per_img][N] ) + residual[M, N]
+//
+// A, B bf16 K-major, fp32 accumulation in TMEM, bf16 or fp32 output.
+// A sources: a 2-D row-major matrix, two matrices concatenated along K
+// (decoder skip concat), or an NHWC activation read through a 4-D TMA box at
+// tap-shifted coordinates (implicit im2col: zero padding comes from TMA
+// out-of-bounds fill, stride-2 from TMA element strides).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sdx {
+
+enum { kActNone = 0, kActSilu = 1, kActRelu = 2, kActGelu = 3 };
+enum { kAMatrix = 0, kAConcat = 1, kAConv = 2 };
+
+struct GemmEpilogue {
+    const float* bias = nullptr;          // [N]
+    const float* bias_img = nullptr;      // [images][N] (time-embedding projection)
+    long long rows_per_img = 1;
+    const __nv_bfloat16* residual = nullptr;  // [M][ld_res]
+    long long ld_res = 0;
+    int act = kActNone;
+    float scale = 1.f;
+    void* out = nullptr;
+    long long ld_out = 0;
+    int out_f32 = 0;
+    const int* rows_dev = nullptr;        // device row-unit count (skip tiles past *rows_dev * rows_per_unit)
+    long long rows_per_unit = 0;
+};
+
+// A prebuilt launch (tensor maps encoded once; replayable / graph-capturable).
+struct GemmPlan {
+    CUtensorMap ta, ta2, tb;
+    int amode = kAMatrix;
+    int M = 0, N = 0, K = 0, K1 = 0;   // K1: split point of the concat source
+    int bn = 128;
+    // conv geometry (amode == kAConv)
+    int H = 0, W = 0, Cin = 0, Ho = 0, Wo = 0, stride = 1, Wt = 0, Ht = 0, Nt = 0;
+    GemmEpilogue epi;
+    bool valid = false;
+};
+
+// Row-major bf16 matrices: A [M][lda] (K used), B [N][ldb].
+GemmPlan plan_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
+                   const GemmEpilogue& epi);
+// A = [A1 (K1 cols) | A2 (K - K1 cols)] per row.
+GemmPlan plan_gemm_concat(const __nv_bfloat16* A1, long long lda1, int K1, const __nv_bfloat16* A2, long long lda2,
+                          const __nv_bfloat16* B, long long ldb, int M, int N, int K, const GemmEpilogue& epi);
+// 3x3 conv, pad 1, stride 1 or 2: x NHWC [imgs][H][W][Cin] bf16, w [Cout][3][3][Cin] bf16,
+// out NHWC [imgs][Ho][Wo][Cout].  Cin % 64 == 0.
+GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, const __nv_bfloat16* w, int Cout,
+                      int stride, const GemmEpilogue& epi);
+
+void run_gemm(const GemmPlan& p, cudaStream_t st);
+
+}  // namespace sdx

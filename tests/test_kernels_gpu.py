@@ -1,0 +1,102 @@
+"""Numerics of the sm_100a tcgen05/TMA kernels of the UNet/TAESD denoiser
+against plain PyTorch fp32 references of the same op (bf16 inputs, fp32
+accumulation).  Tolerance: relative Frobenius error <= 1e-2 and max-abs
+error <= 3e-2 * max|ref| (bf16 output rounding on ~1e2-term dot products)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2312_12491_b200 import _lib
+
+    lib = _lib.lib
+    vp, i64 = C.c_void_p, C.c_int64
+    lib.sdx_kernel_gemm.argtypes = [vp, i64, vp, i64, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
+                                    C.c_float, vp]
+    lib.sdx_kernel_gemm_concat.argtypes = [vp, i64, C.c_int, vp, i64, vp, i64, vp, C.c_int, C.c_int, C.c_int, vp,
+                                           C.c_int, C.c_int, vp]
+    lib.sdx_kernel_conv3x3.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, vp,
+                                       C.c_int, vp, C.c_int, vp]
+    lib.sdx_kernel_last_error.restype = C.c_char_p
+    return lib
+
+
+def ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def check(got, ref, tol=1e-2):
+    got, ref = got.float(), ref.float()
+    rel = (got - ref).norm() / ref.norm().clamp_min(1e-6)
+    mx = (got - ref).abs().max() / ref.abs().max().clamp_min(1e-6)
+    assert rel <= tol and mx <= 3 * tol, (float(rel), float(mx))
+
+
+def act_ref(x, act):
+    return [lambda v: v, torch.nn.functional.silu, torch.relu, torch.nn.functional.gelu][act](x)
+
+
+@pytest.mark.parametrize("shape", [(256, 320, 320), (300, 640, 1280), (128, 64, 64), (4096, 1280, 2560),
+                                   (77, 320, 1024), (1000, 256, 192)])
+@pytest.mark.parametrize("act", [0, 1, 3])
+@pytest.mark.parametrize("out_f32", [0, 1])
+def test_gemm_tc(K, shape, act, out_f32):
+    M, N, Kd = shape
+    g = torch.Generator(device="cuda").manual_seed(M + N + Kd)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, Kd, device="cuda", generator=g) / Kd ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    res = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.float32 if out_f32 else torch.bfloat16)
+    st = K.sdx_kernel_gemm(ptr(A), Kd, ptr(B), Kd, ptr(out), M, N, Kd, ptr(bias), ptr(res), act, out_f32, 1.0,
+                           stream())
+    assert st == 0, K.sdx_kernel_last_error()
+    torch.cuda.synchronize()
+    ref = act_ref(A.float() @ B.float().T + bias, act) + res.float()
+    check(out, ref)
+
+
+def test_gemm_concat(K):
+    M, N, K1, K2 = 512, 640, 1280, 640
+    A1 = torch.randn(M, K1, device="cuda").bfloat16()
+    A2 = torch.randn(M, K2, device="cuda").bfloat16()
+    B = (torch.randn(N, K1 + K2, device="cuda") / 40).bfloat16()
+    out = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    st = K.sdx_kernel_gemm_concat(ptr(A1), K1, K1, ptr(A2), K2, ptr(B), K1 + K2, ptr(out), M, N, K1 + K2, None, 0, 0,
+                                  stream())
+    assert st == 0, K.sdx_kernel_last_error()
+    torch.cuda.synchronize()
+    check(out, torch.cat([A1, A2], 1).float() @ B.float().T)
+
+
+@pytest.mark.parametrize("imgs,H,Cin,Cout,stride", [(2, 64, 64, 320, 1), (1, 64, 320, 320, 1), (3, 32, 128, 640, 1),
+                                                    (2, 16, 128, 128, 1), (3, 8, 256, 1280, 1), (2, 64, 64, 64, 2),
+                                                    (2, 32, 128, 128, 2), (1, 256, 64, 64, 1), (1, 512, 64, 64, 2)])
+def test_conv3x3(K, imgs, H, Cin, Cout, stride):
+    W = H
+    g = torch.Generator(device="cuda").manual_seed(H * Cin + Cout)
+    x = torch.randn(imgs, H, W, Cin, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(Cout, 3, 3, Cin, device="cuda", generator=g) / (3 * Cin ** 0.5)).bfloat16()
+    bias = torch.randn(Cout, device="cuda", generator=g)
+    bimg = torch.randn(imgs, Cout, device="cuda", generator=g)
+    Ho = H if stride == 1 else H // 2
+    out = torch.empty(imgs, Ho, Ho, Cout, device="cuda", dtype=torch.bfloat16)
+    st = K.sdx_kernel_conv3x3(ptr(x), imgs, H, W, Cin, ptr(w), Cout, stride, ptr(bias), ptr(bimg), None, 1, ptr(out),
+                              0, stream())
+    assert st == 0, K.sdx_kernel_last_error()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.permute(0, 3, 1, 2).float(), w.permute(0, 3, 1, 2).float(), bias, stride, 1)
+    ref = ref + bimg[:, :, None, None]
+    ref = torch.nn.functional.silu(ref).permute(0, 2, 3, 1)
+    check(out, ref)
