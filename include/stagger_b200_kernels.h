@@ -30,6 +30,16 @@ int sdx_kernel_conv3x3(const void* x, int imgs, int H, int W, int Cin, const voi
                        const float* bias, const float* bias_img, const void* residual, int act, void* out,
                        int out_f32, void* stream);
 
+/* Flash attention, head_dim 64, tcgen05: out[img*q_len + i][64h..] = softmax(q k^T * scale) v
+ * per (image, head).  Q rows [images*q_len][ld_q] (head h at q_col0 + 64h); KV rows
+ * [kv_rows_total][ld_kv] with K at k_col0 + 64h and V at v_col0 + 64h; image i reads
+ * KV block kv_index[i] (or i) of kv_rows_per_img rows, kv_len of them valid. */
+int sdx_kernel_attention(const void* q, int64_t q_rows_total, int64_t ld_q, int q_col0, const void* kv,
+                         int64_t kv_rows_total, int64_t ld_kv, int k_col0, int v_col0, void* out, int64_t ld_out,
+                         int images, int heads, int q_len, int kv_len, int kv_rows_per_img, const int* kv_index,
+                         float scale, void* stream);
+const char* sdx_kernel_last_error(void);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,319 @@
+// Flash attention (head_dim 64) on tcgen05 / TMEM / TMA for the UNet's
+// self- and cross-attention (the Stream Batch denoiser's attention blocks).
+//
+// One CTA = 128 queries of one (image row, head).  Warp roles:
+//   warp 0      TMA producer: Q once, K/V blocks of 128 keys into a 2-deep ring
+//   warp 1      TMEM alloc + MMA issuer: S = Q K^T (M128 N128 K64) into one of two
+//               TMEM S buffers; O_part = P V (M128 N64 K128, V as an MN-major
+//               operand) into a TMEM O_part buffer
+//   warps 2..5  softmax: one query row per thread (TMEM lane), online max/sum
+//               in fp32 (exp2), P written to smem as bf16 in the 128-byte
+//               swizzled K-major layout, O accumulated in registers
+// Keys past kv_len and queries past q_len are masked (cross-attention pads 77
+// keys to 128; the 8x8 level has 64 tokens per image).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "attention_sm100.cuh"
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace sdx {
+
+using namespace sm100;
+
+namespace {
+
+constexpr int BQ = 128, BKV = 128, HD = 64;
+constexpr uint32_t TILE_BYTES = 128 * 64 * 2;  // one 128-row x 64-col bf16 tile (16 KB)
+
+__device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
+    const uint32_t a = smem_u32(bar);
+    uint32_t done = 0;
+    const long long t0 = clock64();
+    while (true) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(phase)
+            : "memory");
+        if (done) return;
+        if (clock64() - t0 > (1LL << 33)) {
+            printf("sdx attention: mbarrier watchdog (block %d,%d,%d thread %d)\n", blockIdx.x, blockIdx.y,
+                   blockIdx.z, threadIdx.x);
+            asm volatile("trap;");
+        }
+    }
+}
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+__global__ void __launch_bounds__(192, 1)
+    attn_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, AttnArgs a) {
+    const int qb = blockIdx.x;
+    const int head = blockIdx.y;
+    const int img = blockIdx.z;
+    if (a.rows_dev && img >= *a.rows_dev) return;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                       // 16 KB
+    uint8_t* sK = sQ + TILE_BYTES;            // 2 x 16 KB
+    uint8_t* sV = sK + 2 * TILE_BYTES;        // 2 x 16 KB
+    uint8_t* sP = sV + 2 * TILE_BYTES;        // 2 x 32 KB (two 64-key atoms each)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * TILE_BYTES);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;    // [2]
+    uint64_t* kv_empty = bars + 3;   // [2]
+    uint64_t* s_full = bars + 5;     // [2]
+    uint64_t* p_full = bars + 7;     // [2]
+    uint64_t* o_full = bars + 9;     // [1]
+    uint64_t* o_empty = bars + 10;   // [1]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nkv = (a.kv_len + BKV - 1) / BKV;
+    const int q_row0 = img * a.q_rows_per_img + qb * BQ;
+    const int prompt = a.kv_index ? a.kv_index[img] : img;
+    const int kv_row0 = prompt * a.kv_rows_per_img;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tkv);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 128);
+        }
+        mbar_init(o_full, 1);
+        mbar_init(o_empty, 128);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    // TMEM columns: S0 [0,128), S1 [128,256), O_part [256,320)
+
+    if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(q_full, TILE_BYTES);
+            tma_load_2d(sQ, &tq, q_full, a.q_col0 + head * HD, q_row0);
+            for (int j = 0; j < nkv; ++j) {
+                const int b = j & 1;
+                wait_bar(&kv_empty[b], ((j >> 1) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[b], 2 * TILE_BYTES);
+                tma_load_2d(sK + b * TILE_BYTES, &tkv, &kv_full[b], a.k_col0 + head * HD, kv_row0 + j * BKV);
+                tma_load_2d(sV + b * TILE_BYTES, &tkv, &kv_full[b], a.v_col0 + head * HD, kv_row0 + j * BKV);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = idesc_bf16(128, 128);
+            constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);  // B (= V) MN-major
+            wait_bar(q_full, 0);
+            tc_fence_after();
+            const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ));
+            auto issue_s = [&](int j) {
+                const int b = j & 1;
+                wait_bar(&kv_full[b], (j >> 1) & 1);
+                tc_fence_after();
+                const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + b * TILE_BYTES));
+#pragma unroll
+                for (int k = 0; k < HD / 16; ++k) umma_f16(tmem + b * 128, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
+                umma_commit(&s_full[b]);
+            };
+            issue_s(0);
+            if (nkv > 1) issue_s(1);
+            for (int j = 0; j < nkv; ++j) {
+                const int b = j & 1;
+                wait_bar(&p_full[b], (j >> 1) & 1);  // P_j written (S_b consumed)
+                if (j > 0) wait_bar(o_empty, (j - 1) & 1);  // O_part of j-1 drained
+                tc_fence_after();
+                const uint32_t pbase = smem_u32(sP + b * 2 * TILE_BYTES);
+                const uint32_t vbase = smem_u32(sV + b * TILE_BYTES);
+#pragma unroll
+                for (int k = 0; k < BKV / 16; ++k) {
+                    // A = P: atom k/4 (64 keys each), +32 B per K=16 step; B = V rows k*16.. (2048 B per step)
+                    const uint64_t dp = desc_kmajor_sw128(pbase + (k >> 2) * TILE_BYTES) + 2 * (k & 3);
+                    const uint64_t dv = desc_mnmajor_sw128(vbase + k * 2048, 0);
+                    umma_f16(tmem + 256, dp, dv, idesc_o, k != 0);
+                }
+                umma_commit(&kv_empty[b]);
+                umma_commit(o_full);
+                if (j + 2 < nkv) issue_s(j + 2);
+            }
+        }
+        __syncwarp();
+    } else {
+        // softmax / accumulation warps
+        const int q = warp & 3;
+        const int r = q * 32 + lane;  // query row within the tile == TMEM lane
+        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+        const float sl2 = a.scale * 1.4426950408889634f;
+        float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
+        float o[HD];
+#pragma unroll
+        for (int i = 0; i < HD; ++i) o[i] = 0.f;
+        for (int j = 0; j < nkv; ++j) {
+            const int b = j & 1;
+            wait_bar(&s_full[b], (j >> 1) & 1);
+            tc_fence_after();
+            const int kv_valid = a.kv_len - j * BKV;  // keys valid in this block
+            float mx = -INFINITY;
+#pragma unroll 1
+            for (int c = 0; c < BKV; c += 16) {
+                float v[16];
+                tmem_ld16(tmem + lane_off + b * 128 + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (c + i < kv_valid) mx = fmaxf(mx, v[i]);
+            }
+            const float m_new = fmaxf(m, mx * sl2);
+            const float alpha = exp2f(m - m_new);  // m = -inf on the first block -> 0
+            float sum = 0.f;
+            uint8_t* prow = sP + b * 2 * TILE_BYTES;
+#pragma unroll 1
+            for (int c = 0; c < BKV; c += 16) {
+                float v[16];
+                tmem_ld16(tmem + lane_off + b * 128 + c, v);
+                uint32_t pk[8];
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    const float p0 = (c + i < kv_valid) ? exp2f(v[i] * sl2 - m_new) : 0.f;
+                    const float p1 = (c + i + 1 < kv_valid) ? exp2f(v[i + 1] * sl2 - m_new) : 0.f;
+                    sum += p0 + p1;
+                    pk[i / 2] = pack_bf16(p0, p1);
+                }
+                // swizzled store: atom c/64, row r, 16-byte chunks (c%64)/8 and +1
+                uint8_t* atom = prow + (c >> 6) * TILE_BYTES + r * 128;
+                const int ch0 = ((c & 63) >> 3);
+                *reinterpret_cast<uint4*>(atom + (((ch0) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4*>(atom + (((ch0 + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+            }
+            l = l * alpha + sum;
+            m = m_new;
+            fence_async_smem();
+            tc_fence_before();
+            mbar_arrive(&p_full[b]);
+            if (j > 0) {
+                wait_bar(o_full, (j - 1) & 1);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < HD; c += 16) {
+                    float v[16];
+                    tmem_ld16(tmem + lane_off + 256 + c, v);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * alpha_prev + v[i];
+                }
+                tc_fence_before();
+                mbar_arrive(o_empty);
+            }
+            alpha_prev = alpha;
+        }
+        wait_bar(o_full, (nkv - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < HD; c += 16) {
+            float v[16];
+            tmem_ld16(tmem + lane_off + 256 + c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * alpha_prev + v[i];
+        }
+        const int qi = qb * BQ + r;
+        if (qi < a.q_len) {
+            const float inv = 1.f / l;
+            __nv_bfloat16* op = a.out + static_cast<long long>(q_row0 + r) * a.ld_out + a.out_col0 + head * HD;
+#pragma unroll
+            for (int c = 0; c < HD; c += 8) {
+                uint4 w;
+                w.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
+                w.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
+                w.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
+                w.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
+                *reinterpret_cast<uint4*>(op + c) = w;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+void encode_rows(CUtensorMap* m, const void* ptr, long long rows, long long cols, long long ld) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            raise(SDX_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 2)};
+    const cuuint32_t box[2] = {64, 128};
+    const cuuint32_t es[2] = {1, 1};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) raise(SDX_CUDA_ERROR, "attention tensor map encode failed");
+}
+
+}  // namespace
+
+AttnPlan plan_attention(const __nv_bfloat16* q, long long q_rows_total, long long ld_q, int q_col0,
+                        const __nv_bfloat16* kv, long long kv_rows_total, long long ld_kv, int k_col0, int v_col0,
+                        __nv_bfloat16* out, long long ld_out, int out_col0, int images, int heads, int q_len,
+                        int q_rows_per_img, int kv_len, int kv_rows_per_img, const int* kv_index, const int* rows_dev,
+                        float scale) {
+    AttnPlan p;
+    encode_rows(&p.tq, q, q_rows_total, ld_q, ld_q);
+    encode_rows(&p.tkv, kv, kv_rows_total, ld_kv, ld_kv);
+    p.a.q_col0 = q_col0;
+    p.a.k_col0 = k_col0;
+    p.a.v_col0 = v_col0;
+    p.a.out = out;
+    p.a.ld_out = ld_out;
+    p.a.out_col0 = out_col0;
+    p.a.q_len = q_len;
+    p.a.q_rows_per_img = q_rows_per_img;
+    p.a.kv_len = kv_len;
+    p.a.kv_rows_per_img = kv_rows_per_img;
+    p.a.kv_index = kv_index;
+    p.a.rows_dev = rows_dev;
+    p.a.scale = scale;
+    p.images = images;
+    p.heads = heads;
+    p.valid = true;
+    return p;
+}
+
+void run_attention(const AttnPlan& p, cudaStream_t st) {
+    static bool attr = false;
+    const size_t smem = 9 * TILE_BYTES + 1024 + 256;
+    if (!attr) {
+        SDX_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        attr = true;
+    }
+    dim3 grid((p.a.q_len + BQ - 1) / BQ, p.heads, p.images);
+    attn_kernel<<<grid, 192, smem, st>>>(p.tq, p.tkv, p.a);
+    SDX_LAUNCH_CHECK();
+}
+
+}  // namespace sdx

@@ -5,6 +5,7 @@
 #include <string>
 
 #include "common.cuh"
+#include "attention_sm100.cuh"
 #include "gemm_sm100.cuh"
 #include "stagger_b200_kernels.h"
 
@@ -77,6 +78,19 @@ int sdx_kernel_conv3x3(const void* x, int imgs, int H, int W, int Cin, const voi
         auto p = sdx::plan_conv3x3(static_cast<const bf16*>(x), imgs, H, W, Cin, static_cast<const bf16*>(w), Cout,
                                    stride, e);
         sdx::run_gemm(p, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int sdx_kernel_attention(const void* q, int64_t q_rows_total, int64_t ld_q, int q_col0, const void* kv,
+                         int64_t kv_rows_total, int64_t ld_kv, int k_col0, int v_col0, void* out, int64_t ld_out,
+                         int images, int heads, int q_len, int kv_len, int kv_rows_per_img, const int* kv_index,
+                         float scale, void* stream) {
+    return kguard([&] {
+        auto p = sdx::plan_attention(static_cast<const bf16*>(q), q_rows_total, ld_q, q_col0,
+                                     static_cast<const bf16*>(kv), kv_rows_total, ld_kv, k_col0, v_col0,
+                                     static_cast<bf16*>(out), ld_out, 0, images, heads, q_len, q_len, kv_len,
+                                     kv_rows_per_img, kv_index, nullptr, scale);
+        sdx::run_attention(p, static_cast<cudaStream_t>(stream));
     });
 }
 

@@ -100,3 +100,49 @@ def test_conv3x3(K, imgs, H, Cin, Cout, stride):
     ref = ref + bimg[:, :, None, None]
     ref = torch.nn.functional.silu(ref).permute(0, 2, 3, 1)
     check(out, ref)
+
+
+@pytest.fixture(scope="module")
+def KA(K):
+    vp, i64 = C.c_void_p, C.c_int64
+    K.sdx_kernel_attention.argtypes = [vp, i64, i64, C.c_int, vp, i64, i64, C.c_int, C.c_int, vp, i64, C.c_int,
+                                       C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_float, vp]
+    return K
+
+
+@pytest.mark.parametrize("imgs,T,heads", [(2, 4096, 5), (3, 1024, 10), (2, 256, 20), (3, 64, 20), (1, 200, 2)])
+def test_self_attention(KA, imgs, T, heads):
+    Cd = heads * 64
+    g = torch.Generator(device="cuda").manual_seed(T + heads)
+    qkv = torch.randn(imgs * T, 3 * Cd, device="cuda", generator=g).bfloat16()
+    out = torch.zeros(imgs * T, Cd, device="cuda", dtype=torch.bfloat16)
+    st = KA.sdx_kernel_attention(ptr(qkv), imgs * T, 3 * Cd, 0, ptr(qkv), imgs * T, 3 * Cd, Cd, 2 * Cd, ptr(out), Cd,
+                                 imgs, heads, T, T, T, None, 0.125, stream())
+    assert st == 0, KA.sdx_kernel_last_error()
+    torch.cuda.synchronize()
+    q, k, v = qkv.float().view(imgs, T, 3, heads, 64).permute(2, 0, 3, 1, 4)
+    ref = torch.softmax(q @ k.transpose(-1, -2) * 0.125, -1) @ v  # imgs, heads, T, 64
+    check(out, ref.permute(0, 2, 1, 3).reshape(imgs * T, Cd))
+
+
+@pytest.mark.parametrize("T,heads", [(4096, 5), (256, 20)])
+def test_cross_attention(KA, T, heads):
+    # 77 prompt tokens padded to 128 keys; images pick prompt 0 or 1 (cond / negative)
+    imgs, Cd, P = 3, heads * 64, 2
+    g = torch.Generator(device="cuda").manual_seed(7)
+    q = torch.randn(imgs * T, Cd, device="cuda", generator=g).bfloat16()
+    kv = torch.randn(P * 77, 2 * Cd, device="cuda", generator=g).bfloat16()
+    idx = torch.tensor([0, 1, 0], dtype=torch.int32, device="cuda")
+    out = torch.zeros(imgs * T, Cd, device="cuda", dtype=torch.bfloat16)
+    st = KA.sdx_kernel_attention(ptr(q), imgs * T, Cd, 0, ptr(kv), P * 77, 2 * Cd, 0, Cd, ptr(out), Cd, imgs, heads,
+                                 T, 77, 77, ptr(idx), 0.125, stream())
+    assert st == 0, KA.sdx_kernel_last_error()
+    torch.cuda.synchronize()
+    qq = q.float().view(imgs, T, heads, 64).transpose(1, 2)
+    kk = kv.float().view(P, 77, 2, heads, 64)
+    refs = []
+    for i in range(imgs):
+        kp, vp_ = kk[idx[i].item(), :, 0].transpose(0, 1), kk[idx[i].item(), :, 1].transpose(0, 1)
+        refs.append(torch.softmax(qq[i] @ kp.transpose(-1, -2) * 0.125, -1) @ vp_)
+    ref = torch.stack(refs).transpose(1, 2).reshape(imgs * T, Cd)
+    check(out, ref)
