@@ -40,6 +40,22 @@ int sdx_kernel_attention(const void* q, int64_t q_rows_total, int64_t ld_q, int 
                          float scale, void* stream);
 const char* sdx_kernel_last_error(void);
 
+/* The batched UNet denoiser (random-init SD-2.1/SD-turbo topology, bf16
+ * weights, fp32 accumulation) used by the pipeline's predict_eps_batch slot.
+ * taus: timestep of each schedule step; forward() takes rows latents x
+ * (device fp32 [rows][64][64][4], NHWC) with per-row schedule step and prompt
+ * (0 condition, 1 negative) and writes eps (device fp32, same shape). */
+typedef struct sdx_unet sdx_unet;
+int sdx_unet_create(int rmax, const int* taus, int n_steps, uint64_t seed, int device, sdx_unet** out);
+int sdx_unet_destroy(sdx_unet* u);
+int sdx_unet_forward(sdx_unet* u, const float* x, int rows, const int* row_step, const int* row_prompt, float* eps,
+                     void* stream);
+int sdx_unet_param_count(sdx_unet* u, int* n);
+int sdx_unet_param(sdx_unet* u, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32);
+int sdx_unet_flops_per_row(sdx_unet* u, double* flops);
+int sdx_unet_profile(sdx_unet* u, int rows, int cap, const char** kinds, float* ms, int* count);
+int sdx_memcpy_d2d(void* dst, const void* src, int64_t bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -172,7 +172,10 @@ __global__ void __launch_bounds__(192, 1)
         const bool row_ok = row < m_eff;
         const GemmEpilogue& e = g.epi;
         const float* bimg = nullptr;
-        if (e.bias_img && row_ok) bimg = e.bias_img + (static_cast<long long>(row) / e.rows_per_img) * g.N;
+        if (e.bias_img && row_ok) {
+            const long long im = static_cast<long long>(row) / e.rows_per_img;
+            bimg = e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : g.N);
+        }
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
             float v[16];

@@ -24,6 +24,8 @@ struct GemmEpilogue {
     const float* bias = nullptr;          // [N]
     const float* bias_img = nullptr;      // [images][N] (time-embedding projection)
     long long rows_per_img = 1;
+    const int* img_index = nullptr;       // image -> row of bias_img (per-row schedule step) or null
+    long long bias_img_ld = 0;            // row pitch of bias_img (0 = N)
     const __nv_bfloat16* residual = nullptr;  // [M][ld_res]
     long long ld_res = 0;
     int act = kActNone;

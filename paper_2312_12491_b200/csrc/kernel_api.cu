@@ -8,6 +8,8 @@
 #include "attention_sm100.cuh"
 #include "gemm_sm100.cuh"
 #include "stagger_b200_kernels.h"
+#include "unet.cuh"
+#include <vector>
 
 namespace {
 thread_local std::string g_kerr;
@@ -92,6 +94,89 @@ int sdx_kernel_attention(const void* q, int64_t q_rows_total, int64_t ld_q, int 
                                      kv_rows_per_img, kv_index, nullptr, scale);
         sdx::run_attention(p, static_cast<cudaStream_t>(stream));
     });
+}
+
+struct sdx_unet {
+    sdx::UNet* net;
+};
+
+int sdx_unet_create(int rmax, const int* taus, int n_steps, uint64_t seed, int device, sdx_unet** out) {
+    return kguard([&] {
+        SDX_CUDA(cudaSetDevice(device));
+        sdx::UNetConfig c;
+        c.rmax = rmax;
+        c.taus.assign(taus, taus + n_steps);
+        c.seed = seed;
+        *out = new sdx_unet{new sdx::UNet(c, nullptr)};
+    });
+}
+
+int sdx_unet_destroy(sdx_unet* u) {
+    return kguard([&] {
+        if (u) delete u->net;
+        delete u;
+    });
+}
+
+int sdx_unet_forward(sdx_unet* u, const float* x, int rows, const int* row_step, const int* row_prompt, float* eps,
+                     void* stream) {
+    return kguard([&] {
+        auto* n = u->net;
+        const int R = n->config().rmax;
+        if (rows < 1 || rows > R) sdx::raise(SDX_INVALID_ARGUMENT, "unet: rows out of range");
+        cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const size_t elems = static_cast<size_t>(rows) * 64 * 64 * 4;
+        if (x) SDX_CUDA(cudaMemcpyAsync(n->input(), x, elems * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        if (row_step) SDX_CUDA(cudaMemcpyAsync(n->row_step(), row_step, sizeof(int) * rows, cudaMemcpyHostToDevice, st));
+        if (row_prompt)
+            SDX_CUDA(cudaMemcpyAsync(n->row_prompt(), row_prompt, sizeof(int) * rows, cudaMemcpyHostToDevice, st));
+        static thread_local int* d_rows = nullptr;
+        if (!d_rows) SDX_CUDA(cudaMalloc(&d_rows, sizeof(int)));
+        SDX_CUDA(cudaMemcpyAsync(d_rows, &rows, sizeof(int), cudaMemcpyHostToDevice, st));
+        n->forward(d_rows, st);
+        if (eps) SDX_CUDA(cudaMemcpyAsync(eps, n->output(), elems * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        SDX_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int sdx_unet_param_count(sdx_unet* u, int* n) {
+    return kguard([&] { *n = static_cast<int>(u->net->params().size()); });
+}
+
+int sdx_unet_param(sdx_unet* u, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32) {
+    return kguard([&] {
+        const auto& p = u->net->params().at(static_cast<size_t>(i));
+        *name = p.name.c_str();
+        *ptr = p.ptr;
+        *ndim = static_cast<int>(p.shape.size());
+        for (size_t k = 0; k < p.shape.size() && k < 4; ++k) shape[k] = p.shape[k];
+        *is_f32 = p.f32 ? 1 : 0;
+    });
+}
+
+int sdx_unet_flops_per_row(sdx_unet* u, double* flops) {
+    return kguard([&] { *flops = u->net->flops_per_row(); });
+}
+
+// Per-op device times of one forward at `rows` rows: kinds[i] (static strings) and ms[i].
+int sdx_unet_profile(sdx_unet* u, int rows, int cap, const char** kinds, float* ms, int* count) {
+    return kguard([&] {
+        static thread_local int* d_rows = nullptr;
+        static thread_local std::vector<std::pair<std::string, float>> res;
+        if (!d_rows) SDX_CUDA(cudaMalloc(&d_rows, sizeof(int)));
+        SDX_CUDA(cudaMemcpy(d_rows, &rows, sizeof(int), cudaMemcpyHostToDevice));
+        u->net->forward_profiled(d_rows, nullptr, &res);
+        const int n = static_cast<int>(res.size());
+        for (int i = 0; i < n && i < cap; ++i) {
+            kinds[i] = res[static_cast<size_t>(i)].first.c_str();
+            ms[i] = res[static_cast<size_t>(i)].second;
+        }
+        *count = n;
+    });
+}
+
+int sdx_memcpy_d2d(void* dst, const void* src, int64_t bytes) {
+    return kguard([&] { SDX_CUDA(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice)); });
 }
 
 }  // extern "C"

@@ -1,0 +1,428 @@
+// HBM-bound helper kernels of the UNet / TAESD forward: GroupNorm (+SiLU,
+// +channel concat), LayerNorm, GEGLU, nearest upsample, small-channel
+// im2col, timestep embedding, initialisers.  All vectorised over 8 bf16
+// channels (16 B) of NHWC activations; statistics in fp32.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "common.cuh"
+#include "nn_kernels.cuh"
+
+namespace sdx {
+
+namespace {
+
+__device__ __forceinline__ void load8(const bf16* p, float* v) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+
+__device__ __forceinline__ void store8(bf16* p, const float* v) {
+    uint4 u;
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
+
+// ---- GroupNorm ----------------------------------------------------------------
+
+__global__ void gn_stats_kernel(GnPlan p) {
+    const int img = blockIdx.y;
+    if (p.rows_dev && img >= *p.rows_dev) return;
+    extern __shared__ float sm[];  // [2][Ct]
+    const int Ct = p.C1 + p.C2;
+    const int noct = Ct / 8;
+    for (int i = threadIdx.x; i < 2 * Ct; i += blockDim.x) sm[i] = 0.f;
+    __syncthreads();
+    const int per = blockDim.x / noct;  // pixels processed concurrently
+    const int oct = threadIdx.x % noct;
+    const int pl = threadIdx.x / noct;
+    const int pp = (p.HW + p.chunks - 1) / p.chunks;
+    const int pix0 = blockIdx.x * pp;
+    const int pix1 = min(p.HW, pix0 + pp);
+    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0}, q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (pl < per) {
+        const int c = oct * 8;
+        const bool first = c < p.C1;
+        const bf16* base = first ? p.x1 + static_cast<long long>(img) * p.HW * p.C1 + c
+                                 : p.x2 + static_cast<long long>(img) * p.HW * p.C2 + (c - p.C1);
+        const int ld = first ? p.C1 : p.C2;
+        for (int px = pix0 + pl; px < pix1; px += per) {
+            float v[8];
+            load8(base + static_cast<long long>(px) * ld, v);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                s[i] += v[i];
+                q[i] += v[i] * v[i];
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            atomicAdd(&sm[c + i], s[i]);
+            atomicAdd(&sm[Ct + c + i], q[i]);
+        }
+    }
+    __syncthreads();
+    const int cg = Ct / p.groups;
+    for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
+        float a = 0.f, b = 0.f;
+        for (int c = g * cg; c < (g + 1) * cg; ++c) {
+            a += sm[c];
+            b += sm[Ct + c];
+        }
+        float* out = p.partial + ((static_cast<long long>(img) * p.chunks + blockIdx.x) * p.groups + g) * 2;
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+__global__ void gn_apply_kernel(GnPlan p) {
+    const int img = blockIdx.y;
+    if (p.rows_dev && img >= *p.rows_dev) return;
+    __shared__ float mean_s[64], rstd_s[64];
+    const int Ct = p.C1 + p.C2;
+    const int cg = Ct / p.groups;
+    for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < p.chunks; ++k) {
+            const float* pr = p.partial + ((static_cast<long long>(img) * p.chunks + k) * p.groups + g) * 2;
+            a += pr[0];
+            b += pr[1];
+        }
+        const double n = static_cast<double>(cg) * p.HW;
+        const double mean = a / n;
+        double var = b / n - mean * mean;
+        if (var < 0) var = 0;
+        mean_s[g] = static_cast<float>(mean);
+        rstd_s[g] = static_cast<float>(1.0 / sqrt(var + p.eps));
+    }
+    __syncthreads();
+    const int noct = Ct / 8;
+    const int pp = (p.HW + gridDim.x - 1) / gridDim.x;
+    const int pix0 = blockIdx.x * pp;
+    const int pix1 = min(p.HW, pix0 + pp);
+    const long long total = static_cast<long long>(pix1 - pix0) * noct;
+    for (long long idx = threadIdx.x; idx < total; idx += blockDim.x) {
+        const int px = pix0 + static_cast<int>(idx / noct);
+        const int c = static_cast<int>(idx % noct) * 8;
+        const bool first = c < p.C1;
+        const bf16* src = first ? p.x1 + (static_cast<long long>(img) * p.HW + px) * p.C1 + c
+                                : p.x2 + (static_cast<long long>(img) * p.HW + px) * p.C2 + (c - p.C1);
+        float v[8];
+        load8(src, v);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int ch = c + i;
+            const int g = ch / cg;
+            float y = (v[i] - mean_s[g]) * rstd_s[g] * p.gamma[ch] + p.beta[ch];
+            v[i] = p.silu ? silu(y) : y;
+        }
+        store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v);
+    }
+}
+
+// ---- LayerNorm (one warp per row) ------------------------------------------------
+
+template <int MAXV>
+__global__ void layernorm_kernel(const bf16* __restrict__ x, int rows, int C, const float* __restrict__ gamma,
+                                 const float* __restrict__ beta, float eps, bf16* __restrict__ out,
+                                 const int* rows_dev, int rows_per_unit) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    int lim = rows;
+    if (rows_dev) lim = min(lim, *rows_dev * rows_per_unit);
+    if (warp >= lim) return;
+    const bf16* xr = x + static_cast<long long>(warp) * C;
+    const int noct = C / 8;
+    float v[MAXV][8];
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+        const int o = lane + 32 * k;
+        if (o < noct) {
+            load8(xr + o * 8, v[k]);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s += v[k][i];
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    const float mean = s / C;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+        const int o = lane + 32 * k;
+        if (o < noct) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float d = v[k][i] - mean;
+                q += d * d;
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) q += __shfl_xor_sync(0xffffffffu, q, off);
+    const float rstd = rsqrtf(q / C + eps);
+    bf16* orow = out + static_cast<long long>(warp) * C;
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+        const int o = lane + 32 * k;
+        if (o < noct) {
+            float y[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) y[i] = (v[k][i] - mean) * rstd * gamma[o * 8 + i] + beta[o * 8 + i];
+            store8(orow + o * 8, y);
+        }
+    }
+}
+
+// ---- GEGLU ----------------------------------------------------------------------
+
+__global__ void geglu_kernel(const bf16* __restrict__ in, int rows, int H, bf16* __restrict__ out,
+                             const int* rows_dev, int rows_per_unit) {
+    int lim = rows;
+    if (rows_dev) lim = min(lim, *rows_dev * rows_per_unit);
+    const int noct = H / 8;
+    const long long total = static_cast<long long>(lim) * noct;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long r = idx / noct;
+        const int c = static_cast<int>(idx % noct) * 8;
+        float a[8], g[8], y[8];
+        load8(in + r * 2 * H + c, a);
+        load8(in + r * 2 * H + H + c, g);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) y[i] = a[i] * 0.5f * g[i] * (1.f + erff(g[i] * 0.70710678118654752f));
+        store8(out + r * H + c, y);
+    }
+}
+
+// ---- nearest upsample -------------------------------------------------------------
+
+__global__ void upsample_kernel(const bf16* __restrict__ in, int imgs, int H, int W, int C, bf16* __restrict__ out,
+                                const int* rows_dev) {
+    int lim = imgs;
+    if (rows_dev) lim = min(lim, *rows_dev);
+    const int noct = C / 8;
+    const long long total = static_cast<long long>(lim) * 4 * H * W * noct;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int c = static_cast<int>(idx % noct) * 8;
+        long long pix = idx / noct;
+        const int ox = static_cast<int>(pix % (2 * W));
+        pix /= 2 * W;
+        const int oy = static_cast<int>(pix % (2 * H));
+        const long long n = pix / (2 * H);
+        const uint4 v = *reinterpret_cast<const uint4*>(in + ((n * H + oy / 2) * W + ox / 2) * C + c);
+        *reinterpret_cast<uint4*>(out + ((n * 2 * H + oy) * 2 * W + ox) * C + c) = v;
+    }
+}
+
+// ---- im2col for small-channel first convolutions ------------------------------------
+
+template <typename T>
+__global__ void im2col_kernel(const T* __restrict__ in, long long img_stride, const int* img_src, int imgs, int H,
+                              int W, int C, int Kp, float scale, bf16* __restrict__ out, const int* rows_dev) {
+    int lim = imgs;
+    if (rows_dev) lim = min(lim, *rows_dev);
+    const int noct = Kp / 8;
+    const long long total = static_cast<long long>(lim) * H * W * noct;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int k0 = static_cast<int>(idx % noct) * 8;
+        const long long pix = idx / noct;
+        const int x = static_cast<int>(pix % W);
+        const int y = static_cast<int>((pix / W) % H);
+        const int n = static_cast<int>(pix / (static_cast<long long>(W) * H));
+        const int src_img = img_src ? img_src[n] : n;
+        const T* base = in + static_cast<long long>(src_img) * img_stride;
+        float v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = k0 + i;
+            float val = 0.f;
+            if (k < 9 * C) {
+                const int tap = k / C, c = k - tap * C;
+                const int yy = y + tap / 3 - 1, xx = x + tap % 3 - 1;
+                if (yy >= 0 && yy < H && xx >= 0 && xx < W)
+                    val = static_cast<float>(base[(static_cast<long long>(yy) * W + xx) * C + c]) * scale;
+            }
+            v[i] = val;
+        }
+        store8(out + pix * Kp + k0, v);
+    }
+}
+
+// ---- timestep embedding ------------------------------------------------------------
+
+__global__ void temb_kernel(const int* taus, int n, int dim, bf16* out) {
+    const int r = blockIdx.x;
+    const int half = dim / 2;
+    for (int j = threadIdx.x; j < dim; j += blockDim.x) {
+        const int k = j < half ? j : j - half;
+        const float f = expf(-logf(10000.f) * k / half);
+        const float a = static_cast<float>(taus[r]) * f;
+        out[static_cast<long long>(r) * dim + j] = __float2bfloat16(j < half ? cosf(a) : sinf(a));
+    }
+}
+
+// ---- init -----------------------------------------------------------------------------
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ float hash_normal(uint64_t seed, long long i) {
+    const uint64_t a = mix64(seed ^ mix64(static_cast<uint64_t>(i)));
+    const float u1 = (static_cast<float>(a >> 40) + 0.5f) * (1.f / 16777216.f);
+    const float u2 = static_cast<float>((a >> 16) & 0xFFFFFF) * (1.f / 16777216.f);
+    return sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+}
+
+__global__ void fill_normal_bf16_kernel(bf16* p, long long n, float std, uint64_t seed) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        p[i] = __float2bfloat16(std * hash_normal(seed, i));
+}
+__global__ void fill_normal_f32_kernel(float* p, long long n, float std, uint64_t seed) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        p[i] = std * hash_normal(seed, i);
+}
+__global__ void fill_const_kernel(float* p, long long n, float v) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        p[i] = v;
+}
+__global__ void tanh_clamp_kernel(const float* in, float* out, long long n) {
+    for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<long long>(gridDim.x) * blockDim.x)
+        out[i] = tanhf(in[i] / 3.f) * 3.f;
+}
+
+unsigned grid_for(long long work, int threads) {
+    long long b = (work + threads - 1) / threads;
+    if (b > 148LL * 16) b = 148LL * 16;
+    if (b < 1) b = 1;
+    return static_cast<unsigned>(b);
+}
+
+}  // namespace
+
+GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
+                      const float* beta, int silu_, bf16* out, const int* rows_dev) {
+    GnPlan p{};
+    p.x1 = x1;
+    p.x2 = x2;
+    p.C1 = C1;
+    p.C2 = x2 ? C2 : 0;
+    p.HW = HW;
+    p.groups = 32;
+    p.eps = eps;
+    p.gamma = gamma;
+    p.beta = beta;
+    p.silu = silu_;
+    p.out = out;
+    p.imgs = imgs;
+    p.rows_dev = rows_dev;
+    const int Ct = p.C1 + p.C2;
+    if (Ct % 8 != 0 || Ct % p.groups != 0 || (p.C2 && p.C1 % 8 != 0))
+        raise(SDX_INVALID_ARGUMENT, "groupnorm: channels must be multiples of 8 and 32");
+    int chunks = 2 * 148 / (imgs > 0 ? imgs : 1);
+    if (chunks < 4) chunks = 4;
+    if (chunks > HW / 16) chunks = HW / 16 > 0 ? HW / 16 : 1;
+    p.chunks = chunks;
+    p.partial = dev_alloc<float>(static_cast<size_t>(imgs) * chunks * p.groups * 2);
+    return p;
+}
+
+void free_groupnorm(GnPlan& p) {
+    dev_free(p.partial);
+    p.partial = nullptr;
+}
+
+void run_groupnorm(const GnPlan& p, cudaStream_t st) {
+    const int Ct = p.C1 + p.C2;
+    const int noct = Ct / 8;
+    const int threads = noct >= 256 ? noct : noct * (256 / noct);
+    dim3 g1(p.chunks, p.imgs);
+    gn_stats_kernel<<<g1, threads, 2 * Ct * sizeof(float), st>>>(p);
+    SDX_LAUNCH_CHECK();
+    gn_apply_kernel<<<g1, 256, 0, st>>>(p);
+    SDX_LAUNCH_CHECK();
+}
+
+void run_layernorm(const bf16* x, int rows, int C, const float* gamma, const float* beta, float eps, bf16* out,
+                   const int* rows_dev, int rows_per_unit, cudaStream_t st) {
+    const int noct = C / 8;
+    const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
+    if (noct <= 32) layernorm_kernel<1><<<blocks, 256, 0, st>>>(x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
+    else if (noct <= 64) layernorm_kernel<2><<<blocks, 256, 0, st>>>(x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
+    else if (noct <= 160) layernorm_kernel<5><<<blocks, 256, 0, st>>>(x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
+    else raise(SDX_INVALID_ARGUMENT, "layernorm: C too large");
+    SDX_LAUNCH_CHECK();
+}
+
+void run_geglu(const bf16* in, int rows, int H, bf16* out, const int* rows_dev, int rows_per_unit, cudaStream_t st) {
+    geglu_kernel<<<grid_for(static_cast<long long>(rows) * H / 8, 256), 256, 0, st>>>(in, rows, H, out, rows_dev,
+                                                                                       rows_per_unit);
+    SDX_LAUNCH_CHECK();
+}
+
+void run_upsample2x(const bf16* in, int imgs, int H, int W, int C, bf16* out, const int* rows_dev, cudaStream_t st) {
+    upsample_kernel<<<grid_for(static_cast<long long>(imgs) * 4 * H * W * C / 8, 256), 256, 0, st>>>(in, imgs, H, W,
+                                                                                                      C, out, rows_dev);
+    SDX_LAUNCH_CHECK();
+}
+
+void run_im2col3x3_f32(const float* in, int imgs, int H, int W, int C, int Kp, bf16* out, const int* rows_dev,
+                       cudaStream_t st) {
+    im2col_kernel<float><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
+        in, static_cast<long long>(H) * W * C, nullptr, imgs, H, W, C, Kp, 1.f, out, rows_dev);
+    SDX_LAUNCH_CHECK();
+}
+
+void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
+                      int Kp, bf16* out, const int* rows_dev, cudaStream_t st) {
+    im2col_kernel<uint8_t><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
+        in, img_stride, img_src, imgs, H, W, C, Kp, 1.f / 255.f, out, rows_dev);
+    SDX_LAUNCH_CHECK();
+}
+
+void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStream_t st) {
+    temb_kernel<<<n, 128, 0, st>>>(taus, n, dim, out);
+    SDX_LAUNCH_CHECK();
+}
+
+void fill_normal_bf16(bf16* p, long long n, float std, uint64_t seed, cudaStream_t st) {
+    fill_normal_bf16_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n, std, seed);
+    SDX_LAUNCH_CHECK();
+}
+void fill_normal_f32(float* p, long long n, float std, uint64_t seed, cudaStream_t st) {
+    fill_normal_f32_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n, std, seed);
+    SDX_LAUNCH_CHECK();
+}
+void fill_const_f32(float* p, long long n, float v, cudaStream_t st) {
+    fill_const_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n, v);
+    SDX_LAUNCH_CHECK();
+}
+void run_tanh_clamp(const float* in, float* out, long long n, cudaStream_t st) {
+    tanh_clamp_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
+    SDX_LAUNCH_CHECK();
+}
+
+}  // namespace sdx

@@ -1,0 +1,62 @@
+// HBM-bound helper kernels of the UNet / TAESD forward (nn_kernels.cu).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sdx {
+
+using bf16 = __nv_bfloat16;
+
+// GroupNorm over NHWC (optionally over the channel concat [x1 | x2]), 32
+// groups, fp32 statistics, affine, optional SiLU, bf16 out [imgs][HW][C1+C2].
+struct GnPlan {
+    const bf16* x1;
+    const bf16* x2;
+    int C1, C2, HW, groups;
+    float eps;
+    const float *gamma, *beta;
+    int silu;
+    bf16* out;
+    float* partial;  // [imgs][chunks][groups][2]
+    int chunks;
+    int imgs;
+    const int* rows_dev;
+};
+GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
+                      const float* beta, int silu, bf16* out, const int* rows_dev);
+void run_groupnorm(const GnPlan& p, cudaStream_t st);
+void free_groupnorm(GnPlan& p);
+
+// LayerNorm over the last dim C of [rows][C] (fp32 stats), bf16 out.
+void run_layernorm(const bf16* x, int rows, int C, const float* gamma, const float* beta, float eps, bf16* out,
+                   const int* rows_dev, int rows_per_unit, cudaStream_t st);
+
+// GEGLU: out[r][j] = a[r][j] * gelu(g[r][j]) with a = in[:, :H], g = in[:, H:2H]
+void run_geglu(const bf16* in, int rows, int H, bf16* out, const int* rows_dev, int rows_per_unit, cudaStream_t st);
+
+// nearest 2x upsample, NHWC
+void run_upsample2x(const bf16* in, int imgs, int H, int W, int C, bf16* out, const int* rows_dev, cudaStream_t st);
+
+// 3x3/pad1 im2col of a small-channel NHWC input (C <= 7) into [imgs*H*W][Kp] bf16,
+// column = tap*C + c, zero padded to Kp (multiple of 64).  Source is fp32 or u8
+// (u8 scaled by 1/255, the TAESD input range) with an optional per-image gather.
+void run_im2col3x3_f32(const float* in, int imgs, int H, int W, int C, int Kp, bf16* out, const int* rows_dev,
+                       cudaStream_t st);
+void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
+                      int Kp, bf16* out, const int* rows_dev, cudaStream_t st);
+
+// sinusoidal timestep embedding (flip_sin_to_cos, shift 0): [n][dim] bf16
+void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStream_t st);
+
+// deterministic N(0, std) / constant initialisers (counter-based hash RNG)
+void fill_normal_bf16(bf16* p, long long n, float std, uint64_t seed, cudaStream_t st);
+void fill_normal_f32(float* p, long long n, float std, uint64_t seed, cudaStream_t st);
+void fill_const_f32(float* p, long long n, float v, cudaStream_t st);
+
+// elementwise: TAESD decoder input clamp  y = tanh(x / 3) * 3  (fp32 -> fp32)
+void run_tanh_clamp(const float* in, float* out, long long n, cudaStream_t st);
+
+}  // namespace sdx

@@ -1,0 +1,427 @@
+// UNet build + forward (see unet.cuh).
+#include "unet.cuh"
+
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace sdx {
+
+namespace {
+constexpr int kTembIn = 320, kTembDim = 1280;
+constexpr long long kTembTotal = 20160;  // sum of resnet output channels (22 resnets)
+}  // namespace
+
+bf16* UNet::wbf(const std::string& name, std::vector<long long> shape, float std) {
+    long long n = 1;
+    for (auto s : shape) n *= s;
+    bf16* p = dev_alloc<bf16>(static_cast<size_t>(n));
+    allocs_.push_back(p);
+    fill_normal_bf16(p, n, std, cfg_.seed * 1000003ULL + (++param_counter_), nullptr);
+    params_.push_back(Param{name, p, shape, false});
+    return p;
+}
+
+float* UNet::wf32(const std::string& name, std::vector<long long> shape, float std, float constant) {
+    long long n = 1;
+    for (auto s : shape) n *= s;
+    float* p = dev_alloc<float>(static_cast<size_t>(n));
+    allocs_.push_back(p);
+    if (std > 0.f) fill_normal_f32(p, n, std, cfg_.seed * 1000003ULL + (++param_counter_), nullptr);
+    else fill_const_f32(p, n, constant, nullptr);
+    params_.push_back(Param{name, p, shape, true});
+    return p;
+}
+
+bf16* UNet::act(long long elems) {
+    bf16* p = dev_alloc<bf16>(static_cast<size_t>(elems));
+    allocs_.push_back(p);
+    return p;
+}
+
+float* UNet::actf(long long elems) {
+    float* p = dev_alloc<float>(static_cast<size_t>(elems));
+    allocs_.push_back(p);
+    return p;
+}
+
+void UNet::gemm_op(const std::string& kind, const GemmPlan& p) {
+    ops_.push_back(Op{kind, [p](cudaStream_t st) { run_gemm(p, st); }});
+    flops_per_row_ += 2.0 * p.N * p.K * (static_cast<double>(p.M) / R_);
+}
+
+// ResnetBlock2D: GN+SiLU -> conv3x3 (+ time-embedding bias per row) -> GN+SiLU ->
+// conv3x3 + shortcut (identity or 1x1 conv of the concat input).
+bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, int H, int W, const std::string& nm) {
+    const int HW = H * W;
+    const long long M = static_cast<long long>(R_) * HW;
+    const int Cin = Cx + (skip ? Cs : 0);
+    const int* rows = rows_dev_;
+    // norm1 + SiLU over [x | skip]
+    bf16* t1 = act(M * Cin);
+    {
+        float* g = wf32(nm + ".norm1.g", {Cin}, 0.f, 1.f);
+        float* b = wf32(nm + ".norm1.b", {Cin}, 0.f, 0.f);
+        GnPlan gp = plan_groupnorm(x, Cx, skip, Cs, HW, R_, 1e-5f, g, b, 1, t1, rows);
+        gns_.push_back(gp);
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
+    }
+    // conv1 + bias + temb[row_step]
+    bf16* h1 = act(M * Cout);
+    {
+        bf16* w = wbf(nm + ".conv1.w", {Cout, 3, 3, Cin}, 1.f / std::sqrt(9.f * Cin));
+        float* b = wf32(nm + ".conv1.b", {Cout}, 0.02f, 0.f);
+        const long long off = temb_used_;
+        temb_used_ += Cout;
+        params_.push_back(Param{nm + ".temb.w", temb_w_ + off * kTembDim, {Cout, kTembDim}, false});
+        params_.push_back(Param{nm + ".temb.b", temb_b_ + off, {Cout}, true});
+        GemmEpilogue e;
+        e.bias = b;
+        e.bias_img = temb_table_ + off;
+        e.bias_img_ld = kTembTotal;
+        e.img_index = row_step_;
+        e.rows_per_img = HW;
+        e.out = h1;
+        e.rows_dev = rows;
+        e.rows_per_unit = HW;
+        gemm_op("conv3x3", plan_conv3x3(t1, R_, H, W, Cin, w, Cout, 1, e));
+    }
+    bf16* t2 = act(M * Cout);
+    {
+        float* g = wf32(nm + ".norm2.g", {Cout}, 0.f, 1.f);
+        float* b = wf32(nm + ".norm2.b", {Cout}, 0.f, 0.f);
+        GnPlan gp = plan_groupnorm(h1, Cout, nullptr, 0, HW, R_, 1e-5f, g, b, 1, t2, rows);
+        gns_.push_back(gp);
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
+    }
+    const bf16* shortcut = x;
+    if (Cin != Cout || skip) {
+        bf16* s = act(M * Cout);
+        bf16* w = wbf(nm + ".short.w", {Cout, Cin}, 1.f / std::sqrt(static_cast<float>(Cin)));
+        float* b = wf32(nm + ".short.b", {Cout}, 0.02f, 0.f);
+        GemmEpilogue e;
+        e.bias = b;
+        e.out = s;
+        e.rows_dev = rows;
+        e.rows_per_unit = HW;
+        if (skip) gemm_op("conv1x1", plan_gemm_concat(x, Cx, Cx, skip, Cs, w, Cin, static_cast<int>(M), Cout, Cin, e));
+        else gemm_op("conv1x1", plan_gemm(x, Cx, w, Cin, static_cast<int>(M), Cout, Cin, e));
+        shortcut = s;
+    }
+    bf16* out = act(M * Cout);
+    {
+        bf16* w = wbf(nm + ".conv2.w", {Cout, 3, 3, Cout}, 1.f / std::sqrt(9.f * Cout));
+        float* b = wf32(nm + ".conv2.b", {Cout}, 0.02f, 0.f);
+        GemmEpilogue e;
+        e.bias = b;
+        e.residual = shortcut;
+        e.out = out;
+        e.rows_dev = rows;
+        e.rows_per_unit = HW;
+        gemm_op("conv3x3", plan_conv3x3(t2, R_, H, W, Cout, w, Cout, 1, e));
+    }
+    return out;
+}
+
+// Transformer2DModel (linear proj) with one BasicTransformerBlock:
+// GN -> proj_in -> [LN -> self-attn] -> [LN -> cross-attn] -> [LN -> GEGLU FF] -> proj_out + x
+bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& nm) {
+    const int HW = H * W;
+    const long long M = static_cast<long long>(R_) * HW;
+    const int heads = C / 64;
+    const int* rows = rows_dev_;
+    const float wstd = 1.f / std::sqrt(static_cast<float>(C));
+    auto gemm = [&](const std::string& kind, const bf16* a, int K, const bf16* w, int N, const float* bias,
+                    const bf16* res, bf16* out) {
+        GemmEpilogue e;
+        e.bias = bias;
+        e.residual = res;
+        e.out = out;
+        e.rows_dev = rows;
+        e.rows_per_unit = HW;
+        gemm_op(kind, plan_gemm(a, K, w, K, static_cast<int>(M), N, K, e));
+    };
+    auto layernorm = [&](const bf16* in, bf16* out, const std::string& n2) {
+        float* g = wf32(n2 + ".g", {C}, 0.f, 1.f);
+        float* b = wf32(n2 + ".b", {C}, 0.f, 0.f);
+        const int Mi = static_cast<int>(M);
+        ops_.push_back(Op{"layernorm", [=](cudaStream_t st) { run_layernorm(in, Mi, C, g, b, 1e-5f, out, rows, HW, st); }});
+    };
+    bf16* t = act(M * C);
+    {
+        float* g = wf32(nm + ".norm.g", {C}, 0.f, 1.f);
+        float* b = wf32(nm + ".norm.b", {C}, 0.f, 0.f);
+        GnPlan gp = plan_groupnorm(x, C, nullptr, 0, HW, R_, 1e-6f, g, b, 0, t, rows);
+        gns_.push_back(gp);
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
+    }
+    bf16* h = act(M * C);
+    gemm("linear", t, C, wbf(nm + ".proj_in.w", {C, C}, wstd), C, wf32(nm + ".proj_in.b", {C}, 0.02f, 0.f), nullptr, h);
+    // self-attention
+    bf16* n1 = act(M * C);
+    layernorm(h, n1, nm + ".ln1");
+    bf16* qkv = act(M * 3 * C);
+    gemm("linear", n1, C, wbf(nm + ".attn1.qkv.w", {3 * C, C}, wstd), 3 * C, nullptr, nullptr, qkv);
+    bf16* a1 = act(M * C);
+    {
+        AttnPlan ap = plan_attention(qkv, M, 3 * C, 0, qkv, M, 3 * C, C, 2 * C, a1, C, 0, R_, heads, HW, HW, HW, HW,
+                                     nullptr, rows, 0.125f);
+        ops_.push_back(Op{"attention", [ap](cudaStream_t st) { run_attention(ap, st); }});
+        flops_per_row_ += 4.0 * HW * HW * C;
+    }
+    bf16* h2 = act(M * C);
+    gemm("linear", a1, C, wbf(nm + ".attn1.out.w", {C, C}, wstd), C, wf32(nm + ".attn1.out.b", {C}, 0.02f, 0.f), h, h2);
+    // cross-attention against the cached per-prompt K/V
+    bf16* n2 = act(M * C);
+    layernorm(h2, n2, nm + ".ln2");
+    bf16* q = act(M * C);
+    gemm("linear", n2, C, wbf(nm + ".attn2.q.w", {C, C}, wstd), C, nullptr, nullptr, q);
+    bf16* wkv = wbf(nm + ".attn2.kv.w", {2 * C, cfg_.ctx_dim}, 1.f / std::sqrt(static_cast<float>(cfg_.ctx_dim)));
+    const int P = cfg_.n_prompts;
+    bf16* kv = act(static_cast<long long>(P) * cfg_.ctx_len * 2 * C);
+    {
+        GemmEpilogue e;
+        e.out = kv;
+        GemmPlan kp = plan_gemm(ctx_, cfg_.ctx_dim, wkv, cfg_.ctx_dim, P * cfg_.ctx_len, 2 * C, cfg_.ctx_dim, e);
+        ctx_ops_.push_back(Op{"ctx_kv", [kp](cudaStream_t st) { run_gemm(kp, st); }});
+    }
+    bf16* a2 = act(M * C);
+    {
+        AttnPlan ap = plan_attention(q, M, C, 0, kv, static_cast<long long>(P) * cfg_.ctx_len, 2 * C, 0, C, a2, C, 0,
+                                     R_, heads, HW, HW, cfg_.ctx_len, cfg_.ctx_len, row_prompt_, rows, 0.125f);
+        ops_.push_back(Op{"attention", [ap](cudaStream_t st) { run_attention(ap, st); }});
+        flops_per_row_ += 4.0 * HW * cfg_.ctx_len * C;
+    }
+    bf16* h3 = act(M * C);
+    gemm("linear", a2, C, wbf(nm + ".attn2.out.w", {C, C}, wstd), C, wf32(nm + ".attn2.out.b", {C}, 0.02f, 0.f), h2, h3);
+    // GEGLU feed-forward
+    bf16* n3 = act(M * C);
+    layernorm(h3, n3, nm + ".ln3");
+    bf16* ff = act(M * 8 * C);
+    gemm("linear", n3, C, wbf(nm + ".ff1.w", {8 * C, C}, wstd), 8 * C, wf32(nm + ".ff1.b", {8 * C}, 0.02f, 0.f), nullptr, ff);
+    bf16* u = act(M * 4 * C);
+    {
+        const int Mi = static_cast<int>(M);
+        ops_.push_back(Op{"geglu", [=](cudaStream_t st) { run_geglu(ff, Mi, 4 * C, u, rows, HW, st); }});
+    }
+    bf16* h4 = act(M * C);
+    gemm("linear", u, 4 * C, wbf(nm + ".ff2.w", {C, 4 * C}, 1.f / std::sqrt(4.f * C)), C,
+         wf32(nm + ".ff2.b", {C}, 0.02f, 0.f), h3, h4);
+    bf16* out = act(M * C);
+    gemm("linear", h4, C, wbf(nm + ".proj_out.w", {C, C}, wstd), C, wf32(nm + ".proj_out.b", {C}, 0.02f, 0.f), x, out);
+    return out;
+}
+
+bf16* UNet::downsample(const bf16* x, int C, int H, int W, const std::string& nm) {
+    const int Ho = H / 2, Wo = W / 2;
+    bf16* out = act(static_cast<long long>(R_) * Ho * Wo * C);
+    GemmEpilogue e;
+    e.bias = wf32(nm + ".b", {C}, 0.02f, 0.f);
+    e.out = out;
+    e.rows_dev = rows_dev_;
+    e.rows_per_unit = Ho * Wo;
+    gemm_op("conv3x3_s2", plan_conv3x3(x, R_, H, W, C, wbf(nm + ".w", {C, 3, 3, C}, 1.f / std::sqrt(9.f * C)), C, 2, e));
+    return out;
+}
+
+bf16* UNet::upsample(const bf16* x, int C, int H, int W, const std::string& nm) {
+    bf16* up = act(static_cast<long long>(R_) * 4 * H * W * C);
+    const int R = R_;
+    const int* rows = rows_dev_;
+    ops_.push_back(Op{"upsample", [=](cudaStream_t st) { run_upsample2x(x, R, H, W, C, up, rows, st); }});
+    bf16* out = act(static_cast<long long>(R_) * 4 * H * W * C);
+    GemmEpilogue e;
+    e.bias = wf32(nm + ".b", {C}, 0.02f, 0.f);
+    e.out = out;
+    e.rows_dev = rows;
+    e.rows_per_unit = 4 * H * W;
+    gemm_op("conv3x3", plan_conv3x3(up, R_, 2 * H, 2 * W, C, wbf(nm + ".w", {C, 3, 3, C}, 1.f / std::sqrt(9.f * C)), C, 1, e));
+    return out;
+}
+
+UNet::UNet(const UNetConfig& cfg, cudaStream_t st) : cfg_(cfg) {
+    R_ = cfg.rmax;
+    const int H = cfg.H, W = cfg.W;
+    const int n_steps = static_cast<int>(cfg.taus.size());
+    if (n_steps < 1) raise(SDX_INVALID_ARGUMENT, "UNet: empty schedule");
+    SDX_CUDA(cudaDeviceSynchronize());
+    // per-forward inputs / control
+    x_in_ = actf(static_cast<long long>(R_) * H * W * 4);
+    eps_ = actf(static_cast<long long>(R_) * H * W * 4);
+    row_step_ = dev_alloc<int>(static_cast<size_t>(R_));
+    row_prompt_ = dev_alloc<int>(static_cast<size_t>(R_));
+    allocs_.push_back(row_step_);
+    allocs_.push_back(row_prompt_);
+    SDX_CUDA(cudaMemset(row_step_, 0, sizeof(int) * R_));
+    SDX_CUDA(cudaMemset(row_prompt_, 0, sizeof(int) * R_));
+    rows_buf_ = dev_alloc<int>(2);
+    allocs_.push_back(rows_buf_);
+    const int init_rows[2] = {R_, R_};
+    SDX_CUDA(cudaMemcpy(rows_buf_, init_rows, sizeof(init_rows), cudaMemcpyHostToDevice));
+    rows_dev_ = rows_buf_;  // every planned op reads the live row count from rows_buf_[0]
+    ctx_ = act(static_cast<long long>(cfg.n_prompts) * cfg.ctx_len * cfg.ctx_dim);
+    fill_normal_bf16(ctx_, static_cast<long long>(cfg.n_prompts) * cfg.ctx_len * cfg.ctx_dim, 1.f, cfg.seed ^ 0xC0FFEE, nullptr);
+    params_.push_back(Param{"context", ctx_, {cfg.n_prompts, cfg.ctx_len, cfg.ctx_dim}, false});
+
+    // time embedding MLP weights + the concatenated per-resnet projections
+    bf16* t_w1 = wbf("time.linear1.w", {kTembDim, kTembIn}, 1.f / std::sqrt(static_cast<float>(kTembIn)));
+    float* t_b1 = wf32("time.linear1.b", {kTembDim}, 0.02f, 0.f);
+    bf16* t_w2 = wbf("time.linear2.w", {kTembDim, kTembDim}, 1.f / std::sqrt(static_cast<float>(kTembDim)));
+    float* t_b2 = wf32("time.linear2.b", {kTembDim}, 0.02f, 0.f);
+    temb_w_ = dev_alloc<bf16>(static_cast<size_t>(kTembTotal) * kTembDim);
+    temb_b_ = dev_alloc<float>(static_cast<size_t>(kTembTotal));
+    allocs_.push_back(temb_w_);
+    allocs_.push_back(temb_b_);
+    fill_normal_bf16(temb_w_, kTembTotal * kTembDim, 1.f / std::sqrt(static_cast<float>(kTembDim)), cfg.seed ^ 0x7E3B, nullptr);
+    fill_normal_f32(temb_b_, kTembTotal, 0.02f, cfg.seed ^ 0x7E3C, nullptr);
+    temb_table_ = actf(static_cast<long long>(n_steps) * kTembTotal);
+
+    // ---- conv_in: im2col (K = 36 -> 64) + GEMM ----
+    const long long M0 = static_cast<long long>(R_) * H * W;
+    bf16* a0 = act(M0 * 64);
+    {
+        const int R = R_;
+        float* xin = x_in_;
+        const int* rows = rows_dev_;
+        ops_.push_back(Op{"im2col", [=](cudaStream_t s) { run_im2col3x3_f32(xin, R, H, W, 4, 64, a0, rows, s); }});
+    }
+    const int* C = cfg.levels_channels;
+    bf16* h = act(M0 * C[0]);
+    {
+        GemmEpilogue e;
+        e.bias = wf32("conv_in.b", {C[0]}, 0.02f, 0.f);
+        e.out = h;
+        e.rows_dev = rows_dev_;
+        e.rows_per_unit = H * W;
+        bf16* w = wbf("conv_in.w", {C[0], 64}, 1.f / 6.f);  // columns >= 36 multiply zero im2col padding
+        gemm_op("conv_in", plan_gemm(a0, 64, w, 64, static_cast<int>(M0), C[0], 64, e));
+    }
+    struct Skip {
+        const bf16* p;
+        int C;
+    };
+    std::vector<Skip> skips{{h, C[0]}};
+    int cur = C[0], hh = H, ww = W;
+    const bool attn[4] = {true, true, true, false};
+    for (int l = 0; l < 4; ++l) {
+        for (int j = 0; j < 2; ++j) {
+            const std::string nm = "down" + std::to_string(l) + ".res" + std::to_string(j);
+            h = resblock(h, cur, nullptr, 0, C[l], hh, ww, nm);
+            cur = C[l];
+            if (attn[l]) h = transformer(h, cur, hh, ww, "down" + std::to_string(l) + ".attn" + std::to_string(j));
+            skips.push_back({h, cur});
+        }
+        if (l < 3) {
+            h = downsample(h, cur, hh, ww, "down" + std::to_string(l) + ".down");
+            hh /= 2;
+            ww /= 2;
+            skips.push_back({h, cur});
+        }
+    }
+    h = resblock(h, cur, nullptr, 0, cur, hh, ww, "mid.res0");
+    h = transformer(h, cur, hh, ww, "mid.attn0");
+    h = resblock(h, cur, nullptr, 0, cur, hh, ww, "mid.res1");
+    for (int u = 0; u < 4; ++u) {
+        const int l = 3 - u;
+        for (int j = 0; j < 3; ++j) {
+            const Skip sk = skips.back();
+            skips.pop_back();
+            const std::string nm = "up" + std::to_string(u) + ".res" + std::to_string(j);
+            h = resblock(h, cur, sk.p, sk.C, C[l], hh, ww, nm);
+            cur = C[l];
+            if (attn[l]) h = transformer(h, cur, hh, ww, "up" + std::to_string(u) + ".attn" + std::to_string(j));
+        }
+        if (l > 0) {
+            h = upsample(h, cur, hh, ww, "up" + std::to_string(u) + ".up");
+            hh *= 2;
+            ww *= 2;
+        }
+    }
+    // conv_norm_out + SiLU + conv_out (320 -> 4, fp32 eps)
+    bf16* t = act(M0 * cur);
+    {
+        float* g = wf32("norm_out.g", {cur}, 0.f, 1.f);
+        float* b = wf32("norm_out.b", {cur}, 0.f, 0.f);
+        GnPlan gp = plan_groupnorm(h, cur, nullptr, 0, H * W, R_, 1e-5f, g, b, 1, t, rows_dev_);
+        gns_.push_back(gp);
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t s) { run_groupnorm(gp, s); }});
+    }
+    {
+        GemmEpilogue e;
+        e.bias = wf32("conv_out.b", {4}, 0.02f, 0.f);
+        e.out = eps_;
+        e.out_f32 = 1;
+        e.rows_dev = rows_dev_;
+        e.rows_per_unit = H * W;
+        bf16* w = wbf("conv_out.w", {4, 3, 3, cur}, 0.25f / std::sqrt(9.f * cur));
+        gemm_op("conv_out", plan_conv3x3(t, R_, H, W, cur, w, 4, 1, e));
+    }
+    if (temb_used_ != kTembTotal) raise(SDX_LOGIC_ERROR, "UNet: time-embedding slice bookkeeping mismatch");
+
+    // ---- precompute the per-step time-embedding bias table (schedule is fixed) ----
+    {
+        int* taus = dev_alloc<int>(static_cast<size_t>(n_steps));
+        allocs_.push_back(taus);
+        SDX_CUDA(cudaMemcpy(taus, cfg.taus.data(), sizeof(int) * n_steps, cudaMemcpyHostToDevice));
+        bf16* e0 = act(static_cast<long long>(n_steps) * kTembIn);
+        bf16* e1 = act(static_cast<long long>(n_steps) * kTembDim);
+        bf16* e2 = act(static_cast<long long>(n_steps) * kTembDim);
+        run_timestep_embedding(taus, n_steps, kTembIn, e0, st);
+        GemmEpilogue a;
+        a.bias = t_b1;
+        a.act = kActSilu;
+        a.out = e1;
+        run_gemm(plan_gemm(e0, kTembIn, t_w1, kTembIn, n_steps, kTembDim, kTembIn, a), st);
+        GemmEpilogue b;
+        b.bias = t_b2;
+        b.act = kActSilu;  // every consumer applies SiLU(emb) first
+        b.out = e2;
+        run_gemm(plan_gemm(e1, kTembDim, t_w2, kTembDim, n_steps, kTembDim, kTembDim, b), st);
+        GemmEpilogue c;
+        c.bias = temb_b_;
+        c.out = temb_table_;
+        c.out_f32 = 1;
+        run_gemm(plan_gemm(e2, kTembDim, temb_w_, kTembDim, n_steps, static_cast<int>(kTembTotal), kTembDim, c), st);
+    }
+    refresh_context(st);
+    SDX_CUDA(cudaStreamSynchronize(st));
+}
+
+UNet::~UNet() {
+    cudaDeviceSynchronize();
+    for (auto& g : gns_) free_groupnorm(g);
+    for (void* p : allocs_) dev_free(p);
+}
+
+void UNet::refresh_context(cudaStream_t st) {
+    for (auto& op : ctx_ops_) op.fn(st);
+}
+
+void UNet::forward(const int* rows_dev, cudaStream_t st) {
+    if (rows_dev) SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_dev, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    else SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_buf_ + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    for (auto& op : ops_) op.fn(st);
+}
+
+void UNet::forward_profiled(const int* rows_dev, cudaStream_t st, std::vector<std::pair<std::string, float>>* out) {
+    if (rows_dev) SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_dev, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    else SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_buf_ + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    std::vector<cudaEvent_t> ev(ops_.size() + 1);
+    for (auto& e : ev) SDX_CUDA(cudaEventCreate(&e));
+    SDX_CUDA(cudaEventRecord(ev[0], st));
+    for (size_t i = 0; i < ops_.size(); ++i) {
+        ops_[i].fn(st);
+        SDX_CUDA(cudaEventRecord(ev[i + 1], st));
+    }
+    SDX_CUDA(cudaEventSynchronize(ev.back()));
+    out->clear();
+    for (size_t i = 0; i < ops_.size(); ++i) {
+        float ms = 0.f;
+        SDX_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+        out->push_back({ops_[i].kind, ms});
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+}
+
+}  // namespace sdx
