@@ -1,14 +1,18 @@
 #!/usr/bin/env python3
-"""Benchmark of the B200 streaming denoise loop (contract: see DESIGN.md §Measurement).
+"""Benchmark of the B200 streaming denoise loop (contract: DESIGN.md §Measurement).
 
-One step = one pipeline iteration over every stream on every GPU: each stream
-pushes one 3x512x512 u8 frame through the device SSF gate, encode, one batched
-stream-batch tick (n in-flight frames per stream) and decode.  `value` is
-output frames/s with the input frames already resident in HBM; `e2e` is the
-same through the public C-ABI call (sdx_pipeline_push) from pinned host
-frames, with the H2D of the frames and the D2H of the outputs inside the timed
+Headline workload (BASELINE.json configs[1]): img2img Stream Batch with 4
+denoising steps (4 in-flight latents per stream) and TAESD encode/decode of
+3x512x512 frames, random-init SD-2.1/SD-turbo-class UNet, on one B200.
+
+One step = one pipeline iteration of every stream: push one u8 frame per
+stream through the device SSF gate, TAESD encode, one batched UNet call over
+all in-flight rows, the fused R-CFG / LCM step kernel and TAESD decode.
+`value` = output frames/s with the input frames resident in HBM; `e2e` = the
+same through the public C-ABI (sdx_pipeline_push) from pinned host frames,
+with the H2D of the frames and the D2H of the decoded frames in the timed
 region.  Multi-GPU: one process per GPU (torchrun), independent streams per
-GPU, no collective on the data path; time = max over ranks.
+GPU, no collective on the data path; time = max over ranks (weak scaling).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -29,17 +33,20 @@ sys.path.insert(0, ROOT)
 
 H, W, C = 512, 512, 3
 FRAME_BYTES = H * W * C
+LATENT = 4 * 64 * 64
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--steps", type=int, default=40)
+    p.add_argument("--warmup", type=int, default=8)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--streams", type=int, default=8, help="independent streams per GPU")
+    p.add_argument("--streams", type=int, default=1, help="independent streams per GPU")
     p.add_argument("--n-steps", type=int, default=4, help="denoising steps (in-flight frames per stream)")
-    p.add_argument("--guidance", default="self_negative")
+    p.add_argument("--guidance", default="none")
+    p.add_argument("--denoiser", choices=["unet", "analytic"], default="unet")
+    p.add_argument("--no-ssf", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     return p.parse_args()
@@ -119,12 +126,19 @@ class Clocks:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [num(r[0]) for r in self.rows if num(r[0]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        pw = [num(r[2]) for r in self.rows if len(r) > 2 and num(r[2]) is not None]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": num(self.rows[0][1]),
+                "reasons": reasons, "samples": len(self.rows), "power_w_max": max(pw) if pw else None}
 
 
 # ---------------------------------------------------------------------------
@@ -132,9 +146,9 @@ class Clocks:
 # ---------------------------------------------------------------------------
 
 def synthetic_frames(rng, n_iter, S):
-    """Dynamic 512x512 RGB scenes: moving gradient + noise, cosine to the
-    previous frame well below eta, so every frame is processed (the gate still
-    runs its full reduction)."""
+    """Dynamic 512x512 RGB scenes (moving gradients + noise): the cosine to the
+    previous frame stays well below eta, so every frame is processed while the
+    gate still runs its full reduction."""
     yy, xx = np.mgrid[0:H, 0:W]
     out = np.empty((n_iter, S, FRAME_BYTES), dtype=np.uint8)
     for i in range(n_iter):
@@ -148,31 +162,18 @@ def synthetic_frames(rng, n_iter, S):
 def workload_cfg(args):
     from paper_2312_12491_b200 import stagger as sg
 
-    d = FRAME_BYTES  # identity codec: latent = frame (TAESD codec not built yet)
+    unet = args.denoiser == "unet"
+    d = LATENT if unet else FRAME_BYTES
     neg = None
     if args.guidance in ("cfg", "onetime_negative"):
         neg = sg.sample_gaussian(sg.derive_seed(0, 5), d)
     return sg.EngineConfig(n_steps=args.n_steps, guidance_mode=args.guidance, gamma=1.4, delta=1.0,
-                           ssf_enabled=True, eta=0.98, seed=0, d_latent=d, negative_condition=neg)
+                           ssf_enabled=not args.no_ssf, eta=0.98, seed=0, d_latent=d, negative_condition=neg,
+                           backend="unet" if unet else "analytic", codec="taesd" if unet else "identity")
 
 
-def step_bytes_per_launch(n, guidance, d, S):
-    """Algorithmic HBM bytes of one fused step launch at steady state (fp32):
-    per in-flight row: read x (the entering row reads x0 + eps0 instead), the
-    condition mean, eps_cached[next] (not on the terminal row), the reference
-    latent (self: x0 / onetime: x0_ref, cfg: negative mean) and write the result."""
-    per_stream = 0
-    for step in range(n):
-        b = 4 + 4  # mean + write
-        b += 8 if step == 0 else 4
-        if step < n - 1:
-            b += 4
-        if guidance in ("self_negative", "onetime_negative", "cfg"):
-            b += 4
-        if guidance == "onetime_negative" and step == 0:
-            b += 4  # x0_ref write
-        per_stream += b
-    return per_stream * d * S
+def rows_per_frame(n, guidance):
+    return {"cfg": 2 * n, "onetime_negative": n + 1}.get(guidance, n)
 
 
 def run_ours(args, dist: Dist):
@@ -188,6 +189,7 @@ def run_ours(args, dist: Dist):
     rng = np.random.default_rng(1000 + dist.rank)
     frames = synthetic_frames(rng, ring, S)
     p = sg.Pipeline(cfg, S, FRAME_BYTES, ring_depth=ring, device=dev)
+    unet_flops, codec_flops = p.flops()
 
     # ---- value: inputs resident in HBM ----
     p.upload_resident(frames)
@@ -203,24 +205,27 @@ def run_ours(args, dist: Dist):
             p.push_resident(copy_outputs=False)
         ms = p.device_time_ms()
         p.sync()
-    kt = p.kernel_times()
+    stages = p.stage_times()
     ms_max = dist.max(ms)
     frames_out = args.steps * S  # steady state: every stream emits one frame per iteration
 
-    # ---- e2e: public API from pinned host frames, outputs copied back ----
+    # ---- e2e: public API from pinned host frames, decoded frames copied back ----
     hp = C.c_void_p()
     nbytes = frames.nbytes
     assert L.lib.sdx_host_alloc(nbytes, C.byref(hp)) == 0
     host = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(hp.value)).reshape(frames.shape)
     host[:] = frames
+    p.close()
     q = sg.Pipeline(cfg, S, FRAME_BYTES, ring_depth=ring, device=dev)
-    got = 0
     for i in range(args.warmup):
         q.push_ptr(hp.value + (i % ring) * S * FRAME_BYTES)
         for s in range(S):
             q.pop_all(s)
     q.sync()
+    for s in range(S):
+        q.pop_all(s)
     dist.barrier()
+    got = 0
     t0 = time.perf_counter()
     for i in range(args.steps):
         q.push_ptr(hp.value + (i % ring) * S * FRAME_BYTES)
@@ -234,17 +239,37 @@ def run_ours(args, dist: Dist):
     q.close()
     L.lib.sdx_host_free(hp)
 
-    step_ms = kt["step_ms"] / max(1, kt["step_launches"])
-    ssf_ms = kt["ssf_ms"] / max(1, kt["ssf_launches"])
-    algo = step_bytes_per_launch(cfg.n_steps, cfg.guidance_mode, cfg.d_latent, S)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    peak = peaks["hbm_gbs"]
-    achieved = algo / (step_ms * 1e-3) / 1e9
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {}
+    it = max(1, stages["iterations"])
+    rpf = rows_per_frame(cfg.n_steps, cfg.guidance_mode)
     value = dist.world * frames_out / (ms_max * 1e-3)
+    if args.denoiser == "unet":
+        den_ms = stages["denoiser"] / it
+        algo = S * rpf * unet_flops  # FLOPs of one batched UNet call (steady state)
+        achieved = algo / (den_ms * 1e-3) / 1e12
+        peak = peaks.get("bf16_tflops_sustained", 1400.0)
+        roof = {"bound": "tensor", "kernel": "UNet forward (tcgen05 conv/GEMM + flash-attention kernels), "
+                                              f"{S * rpf} rows/launch",
+                "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
+                "traffic": None, "algo_flops_per_launch": algo, "avg_launch_ms": round(den_ms, 4),
+                "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, long loop)"}
+        frame_flops = rpf * unet_flops + codec_flops
+        workload = (f"img2img Stream Batch, {S} stream(s)/GPU x {cfg.n_steps}-step {cfg.guidance_mode}, "
+                    f"TAESD enc/dec 512x512, random-init SD-2.1/SD-turbo UNet (bf16, fp32 accum), "
+                    f"SSF eta 0.98 {'on' if cfg.ssf_enabled else 'off'}")
+        d2h = S * FRAME_BYTES
+    else:
+        den_ms = stages["step"] / it
+        algo = None
+        roof = {"bound": "hbm", "kernel": "fused step kernel", "achieved": None,
+                "peak": peaks.get("hbm_gbs", 6536.4), "unit": "GB/s", "frac": None, "traffic": None}
+        frame_flops = None
+        workload = f"analytic-denoiser pipeline, {S} streams x {cfg.n_steps} steps, identity codec"
+        d2h = S * cfg.d_latent * 4
     line = {
         "metric": "frames/s (img2img 512^2, 1-4 steps)",
-        "value": round(value, 2),
+        "value": round(value, 3),
         "unit": "frames/s",
         "n_gpus": dist.world,
         "steps": args.steps,
@@ -253,28 +278,24 @@ def run_ours(args, dist: Dist):
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "f32",
-        "data": "synthetic 512x512 u8 frames (moving gradients + noise, every frame processed)",
+        "dtype": "bf16" if args.denoiser == "unet" else "f32",
+        "data": "synthetic 512x512 u8 frames (moving gradients + noise), random-init UNet/TAESD weights",
         "config": {
-            "workload": (f"stream-batch pipeline, {S} streams/GPU x {cfg.n_steps}-step {cfg.guidance_mode}, "
-                         "SSF eta 0.98 on, ANALYTIC denoiser (reference parity denoiser) + identity codec; "
-                         "UNet/TAESD not built yet"),
-            "streams_per_gpu": S, "n_steps": cfg.n_steps, "frame": "3x512x512 u8", "latent_elems": cfg.d_latent,
-            "l2": "working set (latents %.0f MB/GPU) > 126 MB L2" % (S * cfg.n_steps * cfg.d_latent * 16 / 1e6),
+            "workload": workload, "streams_per_gpu": S, "n_steps": cfg.n_steps, "guidance": cfg.guidance_mode,
+            "rows_per_tick": S * rpf, "frame": "3x512x512 u8", "latent": "4x64x64",
+            "gflop_per_frame": round(frame_flops / 1e9, 1) if frame_flops else None,
+            "l2": "per-step working set (UNet activations ~%.1f GB) exceeds the 126 MB L2" % (
+                S * rpf * 0.25 if args.denoiser == "unet" else 0.4),
         },
-        "roofline": {"bound": "hbm", "kernel": "step_kernel (fused denoise+R-CFG+LCM update)",
-                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
-                     "algo_bytes_per_launch": algo, "avg_launch_ms": round(step_ms, 5),
-                     "ssf_avg_launch_ms": round(ssf_ms, 5),
-                     "ssf_achieved_gbs": round(2 * FRAME_BYTES * S / (ssf_ms * 1e-3) / 1e9, 1) if ssf_ms else None,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)"},
-        "e2e": {"value": round(dist.world * got / e2e_max, 2), "unit": "frames/s",
-                "h2d_bytes_per_step": S * FRAME_BYTES, "d2h_bytes_per_step": S * cfg.d_latent * 4},
-        "gpu_launches": kt["launches"],
+        "roofline": roof,
+        "stage_ms_per_step": {k: round(stages[k] / it, 4) for k in sg.Pipeline.STAGES},
+        "e2e": {"value": round(dist.world * got / e2e_max, 3), "unit": "frames/s",
+                "h2d_bytes_per_step": S * FRAME_BYTES, "d2h_bytes_per_step": d2h},
+        "gpu_launches": stages["launches"],
         "clocks": clk.summary(),
     }
-    p.close()
+    if frame_flops:
+        line["model_tflops"] = round(frame_flops * frames_out / (ms * 1e-3) / 1e12, 2)
     return line
 
 
@@ -297,11 +318,12 @@ def _cpu_worker(a):
 
 
 def cpu_reference(args, seconds: float, steps: int = 1, warmup: int = 0):
+    """The reference's own CPU path (run_pipeline, analytic denoiser: it has no
+    UNet or TAESD) on the same 3x512x512 frames, one stream per host core."""
     import multiprocessing as mp
 
     cores = os.cpu_count() or 1
     d = FRAME_BYTES
-    # calibrate: one short run on one core
     n_f, dt, which = _cpu_worker((args.n_steps + 2, d, args.n_steps, args.guidance, 0))
     per_frame = dt / n_f
     frames = max(args.n_steps + 1, int(seconds / per_frame / max(1, steps)))
@@ -317,8 +339,9 @@ def cpu_reference(args, seconds: float, steps: int = 1, warmup: int = 0):
     v = float(np.mean(vals))
     return {"value": round(v, 3), "unit": "frames/s", "cores": cores,
             "kind": "reference" if which == "ref" else "port",
-            "sample": (f"{cores} processes x {frames} frames of 3x512x512 (as fp64 payload, identity codec), "
-                       f"run_pipeline deterministic, n={args.n_steps} {args.guidance}, SSF on, analytic denoiser")}
+            "sample": (f"{cores} processes x {frames} frames of 3x512x512 (fp64 payload, identity codec: the "
+                       f"reference has no UNet/TAESD), run_pipeline deterministic, n={args.n_steps} {args.guidance}, "
+                       "SSF on, analytic denoiser")}
 
 
 def main():

@@ -193,8 +193,12 @@ int sdx_pipeline_push_resident(sdx_pipeline* p, int copy_outputs);
  * the SSF reduction and of the fused step kernel since set_profile(1), and the
  * number of library kernel launches issued. */
 int sdx_pipeline_set_profile(sdx_pipeline* p, int on);
-int sdx_pipeline_kernel_times(sdx_pipeline* p, double* ssf_ms, int64_t* ssf_launches, double* step_ms,
-                              int64_t* step_launches, int64_t* total_launches);
+/* ms6: summed device ms per stage over the profiled iterations:
+ * [0] SSF gate, [1] control + reference commit, [2] encode (TAESD), [3] batched
+ * denoiser (UNet), [4] fused step + control end, [5] decode (TAESD). */
+int sdx_pipeline_stage_times(sdx_pipeline* p, double* ms6, int64_t* iterations, int64_t* total_launches);
+/* Algorithmic FLOPs: UNet per denoiser row, TAESD encode + decode per frame (0 if absent). */
+int sdx_pipeline_flops(sdx_pipeline* p, double* unet_per_row, double* codec_per_frame);
 int sdx_pipeline_device_time_ms(sdx_pipeline* p, float* ms); /* since last reset */
 int sdx_pipeline_reset_timer(sdx_pipeline* p);
 

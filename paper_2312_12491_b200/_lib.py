@@ -94,8 +94,8 @@ _sig = {
     "sdx_pipeline_upload_resident": (C.c_int, [P, C.c_void_p, C.c_int]),
     "sdx_pipeline_push_resident": (C.c_int, [P, C.c_int]),
     "sdx_pipeline_set_profile": (C.c_int, [P, C.c_int]),
-    "sdx_pipeline_kernel_times": (C.c_int, [P, D, C.POINTER(C.c_int64), D, C.POINTER(C.c_int64),
-                                            C.POINTER(C.c_int64)]),
+    "sdx_pipeline_stage_times": (C.c_int, [P, D, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "sdx_pipeline_flops": (C.c_int, [P, D, D]),
     "sdx_derive_seed": (C.c_uint64, [C.c_uint64, C.c_uint64]),
     "sdx_build_schedule": (C.c_int, [C.c_int, C.c_int, C.c_double, C.POINTER(sdx_step)]),
     "sdx_sample_gaussian": (C.c_int, [C.c_uint64, C.c_int64, D]),

@@ -261,18 +261,21 @@ int sdx_pipeline_set_profile(sdx_pipeline* p, int on) {
         p->impl.set_profile(on != 0);
     });
 }
-int sdx_pipeline_kernel_times(sdx_pipeline* p, double* ssf_ms, int64_t* ssf_launches, double* step_ms,
-                              int64_t* step_launches, int64_t* total_launches) {
+int sdx_pipeline_stage_times(sdx_pipeline* p, double* ms6, int64_t* iterations, int64_t* total_launches) {
     return guarded([&] {
         NEED(p);
-        double a = 0, b = 0;
-        long long na = 0, nb = 0;
-        p->impl.kernel_times(&a, &na, &b, &nb);
-        if (ssf_ms) *ssf_ms = a;
-        if (ssf_launches) *ssf_launches = na;
-        if (step_ms) *step_ms = b;
-        if (step_launches) *step_launches = nb;
+        NEED(ms6);
+        long long it = 0;
+        p->impl.stage_times(ms6, &it);
+        if (iterations) *iterations = it;
         if (total_launches) *total_launches = p->impl.launches();
+    });
+}
+int sdx_pipeline_flops(sdx_pipeline* p, double* unet_per_row, double* codec_per_frame) {
+    return guarded([&] {
+        NEED(p);
+        if (unet_per_row) *unet_per_row = p->impl.unet_flops_per_row();
+        if (codec_per_frame) *codec_per_frame = p->impl.taesd_flops();
     });
 }
 

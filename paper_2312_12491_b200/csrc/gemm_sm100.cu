@@ -62,6 +62,77 @@ __device__ __forceinline__ float act_fn(float v, int act) {
     }
 }
 
+// bias / per-image bias / residual / activation on 16 accumulator columns of
+// one row, then a bf16, fp32 or u8 store.
+__device__ __forceinline__ void epilogue16(const GemmEpilogue& e, int N, long long row, long long orow, int col0,
+                                           const float* bimg, float* v) {
+    const bool full16 = col0 + 16 <= N;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int col = col0 + i;
+        float x = v[i] * e.scale;
+        if (full16 || col < N) {
+            if (e.bias) x += e.bias[col];
+            if (bimg) x += bimg[col];
+        }
+        v[i] = x;
+    }
+    if (!e.act_after_residual) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = act_fn(v[i], e.act);
+    }
+    if (e.residual) {
+        const __nv_bfloat16* rp = e.residual + row * e.ld_res + col0;
+        if (full16) {
+            const uint4 r0 = *reinterpret_cast<const uint4*>(rp);
+            const uint4 r1 = *reinterpret_cast<const uint4*>(rp + 8);
+            const __nv_bfloat16* rb0 = reinterpret_cast<const __nv_bfloat16*>(&r0);
+            const __nv_bfloat16* rb1 = reinterpret_cast<const __nv_bfloat16*>(&r1);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                v[i] += __bfloat162float(rb0[i]);
+                v[8 + i] += __bfloat162float(rb1[i]);
+            }
+        } else {
+            for (int i = 0; i < 16 && col0 + i < N; ++i) v[i] += __bfloat162float(rp[i]);
+        }
+    }
+    if (e.act_after_residual) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = act_fn(v[i], e.act);
+    }
+    if (e.out_f32 == 1) {
+        float* op = reinterpret_cast<float*>(e.out) + orow * e.ld_out + col0;
+        if (full16) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        } else {
+            for (int i = 0; i < 16 && col0 + i < N; ++i) op[i] = v[i];
+        }
+    } else if (e.out_f32 == 2) {
+        uint8_t* op = reinterpret_cast<uint8_t*>(e.out) + orow * e.ld_out + col0;
+        for (int i = 0; i < 16 && col0 + i < N; ++i)
+            op[i] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(v[i], 0.f), 1.f) * 255.f));
+    } else {
+        __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + orow * e.ld_out + col0;
+        if (full16) {
+            uint4 o0, o1;
+            o0.x = pack_bf16(v[0], v[1]);
+            o0.y = pack_bf16(v[2], v[3]);
+            o0.z = pack_bf16(v[4], v[5]);
+            o0.w = pack_bf16(v[6], v[7]);
+            o1.x = pack_bf16(v[8], v[9]);
+            o1.y = pack_bf16(v[10], v[11]);
+            o1.z = pack_bf16(v[12], v[13]);
+            o1.w = pack_bf16(v[14], v[15]);
+            *reinterpret_cast<uint4*>(op) = o0;
+            *reinterpret_cast<uint4*>(op + 8) = o1;
+        } else {
+            for (int i = 0; i < 16 && col0 + i < N; ++i) op[i] = __float2bfloat16(v[i]);
+        }
+    }
+}
+
 template <int BN, int STAGES, int AMODE>
 __global__ void __launch_bounds__(192, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
@@ -172,9 +243,12 @@ __global__ void __launch_bounds__(192, 1)
         const bool row_ok = row < m_eff;
         const GemmEpilogue& e = g.epi;
         const float* bimg = nullptr;
-        if (e.bias_img && row_ok) {
+        long long orow = row;  // destination row (scatter by image when out_img_map is set)
+        if (row_ok) {
             const long long im = static_cast<long long>(row) / e.rows_per_img;
-            bimg = e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : g.N);
+            if (e.bias_img)
+                bimg = e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : g.N);
+            if (e.out_img_map) orow = static_cast<long long>(e.out_img_map[im]) * e.rows_per_img + (row - im * e.rows_per_img);
         }
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
@@ -182,59 +256,7 @@ __global__ void __launch_bounds__(192, 1)
             tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
             const int col0 = n0 + c;
             if (!row_ok || col0 >= g.N) continue;
-            const bool full16 = col0 + 16 <= g.N;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int col = col0 + i;
-                float x = v[i] * e.scale;
-                if (full16 || col < g.N) {
-                    if (e.bias) x += e.bias[col];
-                    if (bimg) x += bimg[col];
-                }
-                v[i] = act_fn(x, e.act);
-            }
-            if (e.residual) {
-                const __nv_bfloat16* rp = e.residual + static_cast<long long>(row) * e.ld_res + col0;
-                if (full16) {
-                    const uint4 r0 = *reinterpret_cast<const uint4*>(rp);
-                    const uint4 r1 = *reinterpret_cast<const uint4*>(rp + 8);
-                    const __nv_bfloat16* rb0 = reinterpret_cast<const __nv_bfloat16*>(&r0);
-                    const __nv_bfloat16* rb1 = reinterpret_cast<const __nv_bfloat16*>(&r1);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        v[i] += __bfloat162float(rb0[i]);
-                        v[8 + i] += __bfloat162float(rb1[i]);
-                    }
-                } else {
-                    for (int i = 0; i < 16 && col0 + i < g.N; ++i) v[i] += __bfloat162float(rp[i]);
-                }
-            }
-            if (e.out_f32) {
-                float* op = reinterpret_cast<float*>(e.out) + static_cast<long long>(row) * e.ld_out + col0;
-                if (full16) {
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                } else {
-                    for (int i = 0; i < 16 && col0 + i < g.N; ++i) op[i] = v[i];
-                }
-            } else {
-                __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + static_cast<long long>(row) * e.ld_out + col0;
-                if (full16) {
-                    uint4 o0, o1;
-                    o0.x = pack_bf16(v[0], v[1]);
-                    o0.y = pack_bf16(v[2], v[3]);
-                    o0.z = pack_bf16(v[4], v[5]);
-                    o0.w = pack_bf16(v[6], v[7]);
-                    o1.x = pack_bf16(v[8], v[9]);
-                    o1.y = pack_bf16(v[10], v[11]);
-                    o1.z = pack_bf16(v[12], v[13]);
-                    o1.w = pack_bf16(v[14], v[15]);
-                    *reinterpret_cast<uint4*>(op) = o0;
-                    *reinterpret_cast<uint4*>(op + 8) = o1;
-                } else {
-                    for (int i = 0; i < 16 && col0 + i < g.N; ++i) op[i] = __float2bfloat16(v[i]);
-                }
-            }
+            epilogue16(e, g.N, row, orow, col0, bimg, v);
         }
     }
     tc_fence_before();

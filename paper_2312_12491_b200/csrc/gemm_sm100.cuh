@@ -32,7 +32,9 @@ struct GemmEpilogue {
     float scale = 1.f;
     void* out = nullptr;
     long long ld_out = 0;
-    int out_f32 = 0;
+    int out_f32 = 0;                      // 0 bf16, 1 fp32, 2 u8 (round(255 * clamp(v, 0, 1)))
+    int act_after_residual = 0;           // act(acc + bias + residual) instead of act(acc + bias) + residual
+    const int* out_img_map = nullptr;     // image -> destination image block of rows_per_img rows (scatter)
     const int* rows_dev = nullptr;        // device row-unit count (skip tiles past *rows_dev * rows_per_unit)
     long long rows_per_unit = 0;
 };

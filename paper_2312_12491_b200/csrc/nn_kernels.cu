@@ -40,11 +40,9 @@ __device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); 
 __global__ void gn_stats_kernel(GnPlan p) {
     const int img = blockIdx.y;
     if (p.rows_dev && img >= *p.rows_dev) return;
-    extern __shared__ float sm[];  // [2][Ct]
+    extern __shared__ float sm[];  // [per][2][Ct] per-thread partials, reduced in a fixed order
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
-    for (int i = threadIdx.x; i < 2 * Ct; i += blockDim.x) sm[i] = 0.f;
-    __syncthreads();
     const int per = blockDim.x / noct;  // pixels processed concurrently
     const int oct = threadIdx.x % noct;
     const int pl = threadIdx.x / noct;
@@ -69,18 +67,19 @@ __global__ void gn_stats_kernel(GnPlan p) {
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            atomicAdd(&sm[c + i], s[i]);
-            atomicAdd(&sm[Ct + c + i], q[i]);
+            sm[(pl * 2) * Ct + c + i] = s[i];
+            sm[(pl * 2 + 1) * Ct + c + i] = q[i];
         }
     }
     __syncthreads();
     const int cg = Ct / p.groups;
     for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
         float a = 0.f, b = 0.f;
-        for (int c = g * cg; c < (g + 1) * cg; ++c) {
-            a += sm[c];
-            b += sm[Ct + c];
-        }
+        for (int k = 0; k < per; ++k)
+            for (int c = g * cg; c < (g + 1) * cg; ++c) {
+                a += sm[(k * 2) * Ct + c];
+                b += sm[(k * 2 + 1) * Ct + c];
+            }
         float* out = p.partial + ((static_cast<long long>(img) * p.chunks + blockIdx.x) * p.groups + g) * 2;
         out[0] = a;
         out[1] = b;
@@ -233,7 +232,8 @@ __global__ void upsample_kernel(const bf16* __restrict__ in, int imgs, int H, in
 
 template <typename T>
 __global__ void im2col_kernel(const T* __restrict__ in, long long img_stride, const int* img_src, int imgs, int H,
-                              int W, int C, int Kp, float scale, bf16* __restrict__ out, const int* rows_dev) {
+                              int W, int C, int Kp, float scale, int tclamp, bf16* __restrict__ out,
+                              const int* rows_dev) {
     int lim = imgs;
     if (rows_dev) lim = min(lim, *rows_dev);
     const int noct = Kp / 8;
@@ -257,6 +257,7 @@ __global__ void im2col_kernel(const T* __restrict__ in, long long img_stride, co
                 const int yy = y + tap / 3 - 1, xx = x + tap % 3 - 1;
                 if (yy >= 0 && yy < H && xx >= 0 && xx < W)
                     val = static_cast<float>(base[(static_cast<long long>(yy) * W + xx) * C + c]) * scale;
+                if (tclamp) val = tanhf(val / 3.f) * 3.f;  // TAESD decoder input Clamp
             }
             v[i] = val;
         }
@@ -360,7 +361,8 @@ void run_groupnorm(const GnPlan& p, cudaStream_t st) {
     const int noct = Ct / 8;
     const int threads = noct >= 256 ? noct : noct * (256 / noct);
     dim3 g1(p.chunks, p.imgs);
-    gn_stats_kernel<<<g1, threads, 2 * Ct * sizeof(float), st>>>(p);
+    const int per = threads / noct;
+    gn_stats_kernel<<<g1, threads, static_cast<size_t>(per) * 2 * Ct * sizeof(float), st>>>(p);
     SDX_LAUNCH_CHECK();
     gn_apply_kernel<<<g1, 256, 0, st>>>(p);
     SDX_LAUNCH_CHECK();
@@ -392,14 +394,21 @@ void run_upsample2x(const bf16* in, int imgs, int H, int W, int C, bf16* out, co
 void run_im2col3x3_f32(const float* in, int imgs, int H, int W, int C, int Kp, bf16* out, const int* rows_dev,
                        cudaStream_t st) {
     im2col_kernel<float><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
-        in, static_cast<long long>(H) * W * C, nullptr, imgs, H, W, C, Kp, 1.f, out, rows_dev);
+        in, static_cast<long long>(H) * W * C, nullptr, imgs, H, W, C, Kp, 1.f, 0, out, rows_dev);
+    SDX_LAUNCH_CHECK();
+}
+
+void run_im2col3x3_f32_gather(const float* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
+                              int Kp, int tanh_clamp, bf16* out, const int* rows_dev, cudaStream_t st) {
+    im2col_kernel<float><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
+        in, img_stride, img_src, imgs, H, W, C, Kp, 1.f, tanh_clamp, out, rows_dev);
     SDX_LAUNCH_CHECK();
 }
 
 void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
                       int Kp, bf16* out, const int* rows_dev, cudaStream_t st) {
     im2col_kernel<uint8_t><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
-        in, img_stride, img_src, imgs, H, W, C, Kp, 1.f / 255.f, out, rows_dev);
+        in, img_stride, img_src, imgs, H, W, C, Kp, 1.f / 255.f, 0, out, rows_dev);
     SDX_LAUNCH_CHECK();
 }
 

@@ -45,6 +45,8 @@ void run_upsample2x(const bf16* in, int imgs, int H, int W, int C, bf16* out, co
 // (u8 scaled by 1/255, the TAESD input range) with an optional per-image gather.
 void run_im2col3x3_f32(const float* in, int imgs, int H, int W, int C, int Kp, bf16* out, const int* rows_dev,
                        cudaStream_t st);
+void run_im2col3x3_f32_gather(const float* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
+                              int Kp, int tanh_clamp, bf16* out, const int* rows_dev, cudaStream_t st);
 void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
                       int Kp, bf16* out, const int* rows_dev, cudaStream_t st);
 

@@ -433,10 +433,12 @@ Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const 
     if (!errs.empty()) raise(SDX_INVALID_ARGUMENT, errs);
     if (e.cross_frame_attention) raise(SDX_UNSUPPORTED, "cross_frame_attention is not built (SURVEY §8f)");
     if (S_ < 1 || S_ > 1024) raise(SDX_INVALID_ARGUMENT, "n_streams must lie in [1,1024]");
-    if (e.backend != SDX_BACKEND_ANALYTIC) raise(SDX_UNSUPPORTED, "UNet backend not available in this build");
-    if (e.codec != SDX_CODEC_IDENTITY) raise(SDX_UNSUPPORTED, "TAESD codec not available in this build");
     if (e.codec == SDX_CODEC_IDENTITY && D_ != d_)
         raise(SDX_INVALID_ARGUMENT, "LatentCodec::encode: dim mismatch");
+    if (e.codec == SDX_CODEC_TAESD && (D_ != 3LL * 512 * 512 || d_ != 4LL * 64 * 64))
+        raise(SDX_INVALID_ARGUMENT, "TAESD codec: frames are 3x512x512 u8 and latents 4x64x64");
+    if (e.backend == SDX_BACKEND_UNET && d_ != 4LL * 64 * 64)
+        raise(SDX_INVALID_ARGUMENT, "UNet backend: d_latent must be 4x64x64 = 16384");
     const bool needs_neg = e.guidance_mode == SDX_GUIDANCE_CFG || e.guidance_mode == SDX_GUIDANCE_ONETIME_NEGATIVE;
     if (needs_neg && !neg)
         raise(SDX_INVALID_ARGUMENT,
@@ -469,7 +471,47 @@ Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const 
         }
         SDX_CUDA(cudaMemcpy(mt_, words.data(), words.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice));
     }
-    out_bytes_ = d * sizeof(float);
+    const bool taesd = e.codec == SDX_CODEC_TAESD;
+    out_bytes_ = taesd ? static_cast<size_t>(D_) : d * sizeof(float);
+    if (taesd || e.backend == SDX_BACKEND_UNET) {
+        lists_buf_ = dev_alloc<int>(static_cast<size_t>(4 * S_ + 2));
+        SDX_CUDA(cudaMemset(lists_buf_, 0, sizeof(int) * (4 * S_ + 2)));
+        lists_.enc_src = lists_buf_;
+        lists_.enc_dst = lists_buf_ + S_;
+        lists_.dec_src = lists_buf_ + 2 * S_;
+        lists_.dec_dst = lists_buf_ + 3 * S_;
+        lists_.n_ingest = lists_buf_ + 4 * S_;
+        lists_.n_emit = lists_buf_ + 4 * S_ + 1;
+    }
+    if (e.backend == SDX_BACKEND_UNET) {
+        // rows per stream: n (none / self), 2n (cfg), n + 1 (onetime)  (engine.cpp:97-118)
+        const int per = e.guidance_mode == SDX_GUIDANCE_CFG ? 2 * n_
+                        : e.guidance_mode == SDX_GUIDANCE_ONETIME_NEGATIVE ? n_ + 1 : n_;
+        unet_rmax_ = S_ * per;
+        UNetConfig uc;
+        uc.rmax = unet_rmax_;
+        for (int i = 0; i < n_; ++i) uc.taus.push_back(steps[i].tau);
+        uc.seed = e.seed ^ 0x5EEDULL;
+        unet_ = std::make_unique<UNet>(uc, stream_);
+        lists_.row_step = unet_->row_step();
+        lists_.row_prompt = unet_->row_prompt();
+    }
+    if (taesd) {
+        d_out_ = dev_alloc<uint8_t>(static_cast<size_t>(K_) * S_ * D_);
+        TaesdIO io;
+        io.frames = d_in_;
+        io.frame_stride = pad_;
+        io.enc_src = lists_.enc_src;
+        io.enc_count = lists_.n_ingest;
+        io.latent_out = dev_.x0;
+        io.enc_dst = lists_.enc_dst;
+        io.latent_in = dev_.emitted;
+        io.dec_src = lists_.dec_src;
+        io.dec_count = lists_.n_emit;
+        io.frames_out = d_out_;
+        io.dec_dst = lists_.dec_dst;
+        taesd_ = std::make_unique<TAESD>(S_, e.seed ^ 0x7AE5DULL, io, stream_);
+    }
     SDX_CUDA(cudaMallocHost(&h_in_, static_cast<size_t>(K_) * S_ * D_));
     SDX_CUDA(cudaMallocHost(&h_out_, static_cast<size_t>(K_) * S_ * out_bytes_));
     SDX_CUDA(cudaMallocHost(&h_log_, static_cast<size_t>(K_) * S_ * sizeof(LogEntry)));
@@ -489,6 +531,10 @@ Pipeline::~Pipeline() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
     if (copy_) cudaStreamSynchronize(copy_);
+    taesd_.reset();
+    unet_.reset();
+    dev_free(lists_buf_);
+    dev_free(d_out_);
     dev_.release();
     dev_free(d_in_);
     dev_free(d_ref_);
@@ -508,6 +554,12 @@ Pipeline::~Pipeline() {
 void Pipeline::launch_iteration(int k, bool frame_present) {
     const auto& e = cfg_.engine;
     uint8_t* frames = d_in_ + static_cast<size_t>(k) * S_ * pad_;
+    const bool taesd = e.codec == SDX_CODEC_TAESD;
+    const bool unet = e.backend == SDX_BACKEND_UNET;
+    auto mark = [&](int i) {
+        if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * kMarks + i], stream_));
+    };
+    mark(0);
     if (frame_present) {
         SDX_CUDA(cudaStreamWaitEvent(stream_, h2d_[static_cast<size_t>(k)], 0));
         if (e.ssf_enabled) {
@@ -520,36 +572,69 @@ void Pipeline::launch_iteration(int k, bool frame_present) {
             a.max_skip = cfg_.max_skip;
             a.ctl = dev_.ctl;
             a.mt_state = mt_;
-            if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 0], stream_));
             launch_ssf_reduce(a, S_, stream_);
-            if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 1], stream_));
+            launches_ += 1;
         }
+        mark(1);
         launch_ctl_begin(dev_.ctl, S_, n_, e.guidance_mode, e.ssf_enabled ? kIngestSsf : kIngestAlways, -1, 1,
                          dev_.rows, dev_.n_rows, dev_.slot_row_c, dev_.slot_row_n, stream_);
-        CommitArgs ca{};
-        ca.frames = frames;
-        ca.frame_stride = pad_;
-        ca.ref = e.ssf_enabled ? d_ref_ : nullptr;
-        ca.D = D_;
-        ca.x0 = dev_.x0;
-        ca.n = n_;
-        ca.d = d_;
-        ca.ctl = dev_.ctl;
-        launch_commit_encode(ca, S_, stream_);
+        launches_ += 1;
+        if (e.ssf_enabled || !taesd) {
+            CommitArgs ca{};
+            ca.frames = frames;
+            ca.frame_stride = pad_;
+            ca.ref = e.ssf_enabled ? d_ref_ : nullptr;
+            ca.D = D_;
+            ca.x0 = taesd ? nullptr : dev_.x0;
+            ca.n = n_;
+            ca.d = d_;
+            ca.ctl = dev_.ctl;
+            launch_commit_encode(ca, S_, stream_);
+            launches_ += 1;
+        }
     } else {
+        mark(1);
         launch_ctl_begin(dev_.ctl, S_, n_, e.guidance_mode, kIngestAlways, -1, 0, dev_.rows, dev_.n_rows,
                          dev_.slot_row_c, dev_.slot_row_n, stream_);
+        launches_ += 1;
     }
-    if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 2], stream_));
-    launch_step(dev_.step_args(), S_, stream_);
-    if (profile_) SDX_CUDA(cudaEventRecord(kt_[static_cast<size_t>(k) * 4 + 3], stream_));
-    launches_ += frame_present ? (cfg_.engine.ssf_enabled ? 5 : 4) : 3;
+    if (taesd || unet) {
+        launch_ctl_lists(dev_.ctl, S_, n_, k, dev_.rows, dev_.n_rows, lists_, stream_);
+        launches_ += 1;
+    }
+    mark(2);
+    if (taesd && frame_present) {
+        taesd_->encode(stream_);
+        launches_ += taesd_->launches_per_encode();
+    }
+    mark(3);
+    StepArgs sa = dev_.step_args();
+    if (unet) {
+        launch_unet_prep(dev_.ctl, dev_.rows, dev_.n_rows, unet_rmax_, n_, d_, dev_.x_cur, dev_.x0, dev_.eps_cached,
+                         dev_.tbl, unet_->input(), stream_);
+        unet_->forward(dev_.n_rows, stream_);
+        launches_ += 1 + unet_->launches_per_forward();
+        sa.eps_ext = unet_->output();
+        sa.eps_ext_stride = d_;
+    }
+    mark(4);
+    launch_step(sa, S_, stream_);
     launch_ctl_end(dev_.ctl, S_, n_, e.guidance_mode, dev_.log, frame_present ? 1 : 0, stream_);
+    launches_ += 2;
+    mark(5);
+    if (taesd) {
+        taesd_->decode(stream_);
+        launches_ += taesd_->launches_per_decode();
+    }
+    mark(6);
     SDX_CUDA(cudaMemcpyAsync(h_log_ + static_cast<size_t>(k) * S_, dev_.log, sizeof(LogEntry) * S_,
                              cudaMemcpyDeviceToHost, stream_));
-    if (!resident_ || copy_outputs_)
-        SDX_CUDA(cudaMemcpyAsync(h_out_ + static_cast<size_t>(k) * S_ * out_bytes_, dev_.emitted,
-                                 out_bytes_ * S_, cudaMemcpyDeviceToHost, stream_));
+    if (!resident_ || copy_outputs_) {
+        const void* src = taesd ? static_cast<const void*>(d_out_ + static_cast<size_t>(k) * S_ * out_bytes_)
+                                : static_cast<const void*>(dev_.emitted);
+        SDX_CUDA(cudaMemcpyAsync(h_out_ + static_cast<size_t>(k) * S_ * out_bytes_, src, out_bytes_ * S_,
+                                 cudaMemcpyDeviceToHost, stream_));
+    }
     SDX_CUDA(cudaEventRecord(done_[static_cast<size_t>(k)], stream_));
 }
 
@@ -578,15 +663,13 @@ void Pipeline::flush_below(StreamHost& h, int64_t limit, std::vector<Out>& stage
 void Pipeline::process(int k, bool frame_present) {
     const auto& e = cfg_.engine;
     if (profile_) {
-        float ms = 0.f;
-        if (frame_present && e.ssf_enabled) {
-            SDX_CUDA(cudaEventElapsedTime(&ms, kt_[static_cast<size_t>(k) * 4 + 0], kt_[static_cast<size_t>(k) * 4 + 1]));
-            ktime_[0] += ms;
-            kcount_[0] += 1;
+        for (int i = 0; i + 1 < kMarks; ++i) {
+            float ms = 0.f;
+            SDX_CUDA(cudaEventElapsedTime(&ms, kt_[static_cast<size_t>(k) * kMarks + i],
+                                          kt_[static_cast<size_t>(k) * kMarks + i + 1]));
+            ktime_[i] += ms;
         }
-        SDX_CUDA(cudaEventElapsedTime(&ms, kt_[static_cast<size_t>(k) * 4 + 2], kt_[static_cast<size_t>(k) * 4 + 3]));
-        ktime_[1] += ms;
-        kcount_[1] += 1;
+        kcount_ += 1;
     }
     const size_t cap8 = static_cast<size_t>(e.queue_capacity) * 8;
     for (int s = 0; s < S_; ++s) {
@@ -819,20 +902,18 @@ void Pipeline::set_profile(bool on) {
     SDX_CUDA(cudaSetDevice(device_));
     sync();
     if (on && kt_.empty()) {
-        kt_.resize(static_cast<size_t>(K_) * 4);
+        kt_.resize(static_cast<size_t>(K_) * kMarks);
         for (auto& ev : kt_) SDX_CUDA(cudaEventCreate(&ev));
     }
     profile_ = on;
-    ktime_[0] = ktime_[1] = 0.0;
-    kcount_[0] = kcount_[1] = 0;
+    for (auto& t : ktime_) t = 0.0;
+    kcount_ = 0;
     launches_ = 0;
 }
 
-void Pipeline::kernel_times(double* ssf_ms, long long* ssf_n, double* step_ms, long long* step_n) const {
-    *ssf_ms = ktime_[0];
-    *ssf_n = kcount_[0];
-    *step_ms = ktime_[1];
-    *step_n = kcount_[1];
+void Pipeline::stage_times(double* ms, long long* iters) const {
+    for (int i = 0; i + 1 < kMarks; ++i) ms[i] = ktime_[i];
+    *iters = kcount_;
 }
 
 float Pipeline::device_time_ms() {

@@ -15,6 +15,9 @@
 #include "common.cuh"
 #include "device_ctl.cuh"
 #include "kernels_core.cuh"
+#include "pipeline_kernels.cuh"
+#include "taesd.cuh"
+#include "unet.cuh"
 
 namespace sdx {
 
@@ -148,11 +151,16 @@ class Pipeline {
     void sync();
     void reset_timer();
     float device_time_ms();
-    // Per-kernel device time (CUDA events around the SSF reduction and the
-    // step kernel, on the launching stream), accumulated while profiling.
+    // Per-stage device time (CUDA events on the pipeline stream between the
+    // stages of every iteration), accumulated while profiling:
+    // [0] SSF, [1] control + commit, [2] encode, [3] denoiser (UNet), [4] step +
+    // control end, [5] decode.
+    static constexpr int kMarks = 7;
     void set_profile(bool on);
-    void kernel_times(double* ssf_ms, long long* ssf_n, double* step_ms, long long* step_n) const;
+    void stage_times(double* ms, long long* iters) const;
     long long launches() const { return launches_; }
+    double unet_flops_per_row() const { return unet_ ? unet_->flops_per_row() : 0.0; }
+    double taesd_flops() const { return taesd_ ? taesd_->enc_flops_per_image() + taesd_->dec_flops_per_image() : 0.0; }
 
   private:
     struct Out {
@@ -200,10 +208,17 @@ class Pipeline {
     std::vector<StreamHost> st_;
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;
     bool profile_ = false;
-    std::vector<cudaEvent_t> kt_;  // [K][4]
-    double ktime_[2] = {0, 0};
-    long long kcount_[2] = {0, 0};
+    std::vector<cudaEvent_t> kt_;  // [K][kMarks]
+    double ktime_[kMarks - 1] = {};
+    long long kcount_ = 0;
     long long launches_ = 0;
+    // UNet backend / TAESD codec
+    std::unique_ptr<UNet> unet_;
+    std::unique_ptr<TAESD> taesd_;
+    int unet_rmax_ = 0;
+    int* lists_buf_ = nullptr;
+    CodecLists lists_{};
+    uint8_t* d_out_ = nullptr;  // [K][S][frame_bytes] decoded frames (TAESD)
 };
 
 }  // namespace sdx

@@ -416,13 +416,23 @@ class Pipeline:
     def set_profile(self, on: bool = True):
         _check(L.lib.sdx_pipeline_set_profile(self._h, int(on)))
 
-    def kernel_times(self) -> dict:
+    STAGES = ("ssf", "control", "encode", "denoiser", "step", "decode")
+
+    def stage_times(self) -> dict:
+        """Summed device ms per pipeline stage since set_profile(True), plus
+        iterations and library kernel launches."""
+        ms = (C.c_double * 6)()
+        it, nl = C.c_int64(), C.c_int64()
+        _check(L.lib.sdx_pipeline_stage_times(self._h, ms, C.byref(it), C.byref(nl)))
+        d = {k: ms[i] for i, k in enumerate(self.STAGES)}
+        d["iterations"] = it.value
+        d["launches"] = nl.value
+        return d
+
+    def flops(self) -> tuple[float, float]:
         a, b = C.c_double(), C.c_double()
-        na, nb, nt = C.c_int64(), C.c_int64(), C.c_int64()
-        _check(L.lib.sdx_pipeline_kernel_times(self._h, C.byref(a), C.byref(na), C.byref(b), C.byref(nb),
-                                               C.byref(nt)))
-        return dict(ssf_ms=a.value, ssf_launches=na.value, step_ms=b.value, step_launches=nb.value,
-                    launches=nt.value)
+        _check(L.lib.sdx_pipeline_flops(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def device_time_ms(self) -> float:
         v = C.c_float()
