@@ -53,32 +53,54 @@ __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-__global__ void __launch_bounds__(192, 1)
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+        "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+        "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+        : "memory");
+}
+
+// Two 128-query tiles per CTA (256 queries of one image/head) share every K/V
+// block.  10 warps: 0 TMA, 1 MMA, 2..5 softmax of tile 0, 6..9 softmax of tile 1.
+// TMEM per tile: S [128 cols] + O [64 cols]; O accumulates across KV blocks in
+// TMEM and is rescaled only when a row max grows by more than 2^8 (lazy
+// rescaling), so P = exp2(s - m_used) stays <= 256 and never overflows.
+__global__ void __launch_bounds__(320, 1)
     attn_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, AttnArgs a) {
-    const int qb = blockIdx.x;
+    const int qp = blockIdx.x;  // pair of q tiles
     const int head = blockIdx.y;
     const int img = blockIdx.z;
     if (a.rows_dev && img >= *a.rows_dev) return;
+    const bool has1 = qp * 2 * BQ + BQ < a.q_len;  // second tile holds live queries
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sQ = smem;                       // 16 KB
-    uint8_t* sK = sQ + TILE_BYTES;            // 2 x 16 KB
+    uint8_t* sQ = smem;                       // 2 x 16 KB
+    uint8_t* sK = sQ + 2 * TILE_BYTES;        // 2 x 16 KB
     uint8_t* sV = sK + 2 * TILE_BYTES;        // 2 x 16 KB
-    uint8_t* sP = sV + 2 * TILE_BYTES;        // 2 x 32 KB (two 64-key atoms each)
+    uint8_t* sP = sV + 2 * TILE_BYTES;        // 2 tiles x 32 KB (two 64-key atoms each)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * TILE_BYTES);
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;    // [2]
     uint64_t* kv_empty = bars + 3;   // [2]
-    uint64_t* s_full = bars + 5;     // [2]
-    uint64_t* p_full = bars + 7;     // [2]
-    uint64_t* o_full = bars + 9;     // [1]
-    uint64_t* o_empty = bars + 10;   // [1]
+    uint64_t* s_full = bars + 5;     // [2] per tile
+    uint64_t* p_full = bars + 7;     // [2] per tile
+    uint64_t* pv_done = bars + 9;    // [2] per tile
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkv = (a.kv_len + BKV - 1) / BKV;
-    const int q_row0 = img * a.q_rows_per_img + qb * BQ;
+    const int q_row0 = img * a.q_rows_per_img + qp * 2 * BQ;
     const int prompt = a.kv_index ? a.kv_index[img] : img;
     const int kv_row0 = prompt * a.kv_rows_per_img;
 
@@ -91,9 +113,8 @@ __global__ void __launch_bounds__(192, 1)
             mbar_init(&kv_empty[i], 1);
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 128);
+            mbar_init(&pv_done[i], 1);
         }
-        mbar_init(o_full, 1);
-        mbar_init(o_empty, 128);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -101,12 +122,13 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    // TMEM columns: S0 [0,128), S1 [128,256), O_part [256,320)
+    // TMEM columns: tile t: S at t*192, O at t*192 + 128
 
     if (warp == 0) {
         if (lane == 0) {
-            mbar_expect_tx(q_full, TILE_BYTES);
+            mbar_expect_tx(q_full, (has1 ? 2 : 1) * TILE_BYTES);
             tma_load_2d(sQ, &tq, q_full, a.q_col0 + head * HD, q_row0);
+            if (has1) tma_load_2d(sQ + TILE_BYTES, &tq, q_full, a.q_col0 + head * HD, q_row0 + BQ);
             for (int j = 0; j < nkv; ++j) {
                 const int b = j & 1;
                 wait_bar(&kv_empty[b], ((j >> 1) & 1) ^ 1);
@@ -119,127 +141,129 @@ __global__ void __launch_bounds__(192, 1)
         if (lane == 0) {
             constexpr uint32_t idesc_s = idesc_bf16(128, 128);
             constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);  // B (= V) MN-major
+            const int ntile = has1 ? 2 : 1;
             wait_bar(q_full, 0);
             tc_fence_after();
-            const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ));
-            auto issue_s = [&](int j) {
-                const int b = j & 1;
-                wait_bar(&kv_full[b], (j >> 1) & 1);
-                tc_fence_after();
-                const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + b * TILE_BYTES));
+            auto issue_s = [&](int t, int j) {
+                const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ + t * TILE_BYTES));
+                const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + (j & 1) * TILE_BYTES));
 #pragma unroll
-                for (int k = 0; k < HD / 16; ++k) umma_f16(tmem + b * 128, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
-                umma_commit(&s_full[b]);
+                for (int k = 0; k < HD / 16; ++k) umma_f16(tmem + t * 192, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
+                umma_commit(&s_full[t]);
             };
-            issue_s(0);
-            if (nkv > 1) issue_s(1);
-            for (int j = 0; j < nkv; ++j) {
-                const int b = j & 1;
-                wait_bar(&p_full[b], (j >> 1) & 1);  // P_j written (S_b consumed)
-                if (j > 0) wait_bar(o_empty, (j - 1) & 1);  // O_part of j-1 drained
-                tc_fence_after();
-                const uint32_t pbase = smem_u32(sP + b * 2 * TILE_BYTES);
-                const uint32_t vbase = smem_u32(sV + b * TILE_BYTES);
+            auto issue_pv = [&](int t, int j) {
+                const uint32_t pbase = smem_u32(sP + t * 2 * TILE_BYTES);
+                const uint32_t vbase = smem_u32(sV + (j & 1) * TILE_BYTES);
 #pragma unroll
                 for (int k = 0; k < BKV / 16; ++k) {
-                    // A = P: atom k/4 (64 keys each), +32 B per K=16 step; B = V rows k*16.. (2048 B per step)
                     const uint64_t dp = desc_kmajor_sw128(pbase + (k >> 2) * TILE_BYTES) + 2 * (k & 3);
                     const uint64_t dv = desc_mnmajor_sw128(vbase + k * 2048, 0);
-                    umma_f16(tmem + 256, dp, dv, idesc_o, k != 0);
+                    umma_f16(tmem + t * 192 + 128, dp, dv, idesc_o, (j > 0 || k != 0) ? 1u : 0u);
                 }
-                umma_commit(&kv_empty[b]);
-                umma_commit(o_full);
-                if (j + 2 < nkv) issue_s(j + 2);
+                umma_commit(&pv_done[t]);
+            };
+            wait_bar(&kv_full[0], 0);
+            tc_fence_after();
+            for (int t = 0; t < ntile; ++t) issue_s(t, 0);
+            for (int j = 0; j < nkv; ++j) {
+                const bool more = j + 1 < nkv;
+                if (more) {
+                    wait_bar(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+                }
+                for (int t = 0; t < ntile; ++t) {
+                    wait_bar(&p_full[t], j & 1);  // P_t(j) in smem, S_t consumed, O_t rescaled
+                    tc_fence_after();
+                    if (more) issue_s(t, j + 1);
+                    issue_pv(t, j);
+                }
+                umma_commit(&kv_empty[j & 1]);
             }
         }
         __syncwarp();
     } else {
-        // softmax / accumulation warps
+        const int t = (warp - 2) >> 2;  // q tile of this softmax warpgroup
         const int q = warp & 3;
-        const int r = q * 32 + lane;  // query row within the tile == TMEM lane
-        const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-        const float sl2 = a.scale * 1.4426950408889634f;
-        float m = -INFINITY, l = 0.f, alpha_prev = 1.f;
-        float o[HD];
-#pragma unroll
-        for (int i = 0; i < HD; ++i) o[i] = 0.f;
-        for (int j = 0; j < nkv; ++j) {
-            const int b = j & 1;
-            wait_bar(&s_full[b], (j >> 1) & 1);
-            tc_fence_after();
-            const int kv_valid = a.kv_len - j * BKV;  // keys valid in this block
-            float mx = -INFINITY;
-#pragma unroll 1
-            for (int c = 0; c < BKV; c += 16) {
-                float v[16];
-                tmem_ld16(tmem + lane_off + b * 128 + c, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (c + i < kv_valid) mx = fmaxf(mx, v[i]);
-            }
-            const float m_new = fmaxf(m, mx * sl2);
-            const float alpha = exp2f(m - m_new);  // m = -inf on the first block -> 0
-            float sum = 0.f;
-            uint8_t* prow = sP + b * 2 * TILE_BYTES;
-#pragma unroll 1
-            for (int c = 0; c < BKV; c += 16) {
-                float v[16];
-                tmem_ld16(tmem + lane_off + b * 128 + c, v);
-                uint32_t pk[8];
-#pragma unroll
-                for (int i = 0; i < 16; i += 2) {
-                    const float p0 = (c + i < kv_valid) ? exp2f(v[i] * sl2 - m_new) : 0.f;
-                    const float p1 = (c + i + 1 < kv_valid) ? exp2f(v[i + 1] * sl2 - m_new) : 0.f;
-                    sum += p0 + p1;
-                    pk[i / 2] = pack_bf16(p0, p1);
-                }
-                // swizzled store: atom c/64, row r, 16-byte chunks (c%64)/8 and +1
-                uint8_t* atom = prow + (c >> 6) * TILE_BYTES + r * 128;
-                const int ch0 = ((c & 63) >> 3);
-                *reinterpret_cast<uint4*>(atom + (((ch0) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                *reinterpret_cast<uint4*>(atom + (((ch0 + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-            }
-            l = l * alpha + sum;
-            m = m_new;
-            fence_async_smem();
-            tc_fence_before();
-            mbar_arrive(&p_full[b]);
-            if (j > 0) {
-                wait_bar(o_full, (j - 1) & 1);
+        const int r = q * 32 + lane;
+        if (t == 0 || has1) {
+            const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+            const uint32_t s_addr = tmem + lane_off + t * 192;
+            const uint32_t o_addr = s_addr + 128;
+            const float sl2 = a.scale * 1.4426950408889634f;
+            float m_used = -INFINITY, l = 0.f;
+            uint8_t* prow = sP + t * 2 * TILE_BYTES;
+            for (int j = 0; j < nkv; ++j) {
+                wait_bar(&s_full[t], j & 1);
                 tc_fence_after();
+                uint32_t sr[128];
+                tmem_ld32_nowait(s_addr + 0, sr);
+                tmem_ld32_nowait(s_addr + 32, sr + 32);
+                tmem_ld32_nowait(s_addr + 64, sr + 64);
+                tmem_ld32_nowait(s_addr + 96, sr + 96);
+                tmem_wait_ld();
+                const int kv_valid = a.kv_len - j * BKV;
+                float mx = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < HD; c += 16) {
-                    float v[16];
-                    tmem_ld16(tmem + lane_off + 256 + c, v);
+                for (int i = 0; i < BKV; ++i)
+                    if (i < kv_valid) mx = fmaxf(mx, __uint_as_float(sr[i]));
+                const float m_row = mx * sl2;
+                if (j > 0) wait_bar(&pv_done[t], (j - 1) & 1);  // PV(j-1) finished reading P_t and writing O_t
+                if (m_row > m_used + 8.f) {
+                    // lazy rescale: new reference max for this row
+                    const float m_new = m_row;
+                    const float corr = ex2(m_used - m_new);  // m_used = -inf -> 0
+                    if (j > 0) {
+                        tc_fence_after();
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * alpha_prev + v[i];
+                        for (int c = 0; c < HD; c += 16) {
+                            float v[16];
+                            tmem_ld16(o_addr + c, v);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) v[i] *= corr;
+                            tmem_st16(o_addr + c, v);
+                        }
+                    }
+                    l *= corr;
+                    m_used = m_new;
                 }
+                float sum = 0.f;
+#pragma unroll
+                for (int c = 0; c < BKV; c += 16) {
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int i = 0; i < 16; i += 2) {
+                        const float p0 = (c + i < kv_valid) ? ex2(fmaf(__uint_as_float(sr[c + i]), sl2, -m_used)) : 0.f;
+                        const float p1 = (c + i + 1 < kv_valid) ? ex2(fmaf(__uint_as_float(sr[c + i + 1]), sl2, -m_used)) : 0.f;
+                        sum += p0 + p1;
+                        pk[i / 2] = pack_bf16(p0, p1);
+                    }
+                    uint8_t* atom = prow + (c >> 6) * TILE_BYTES + r * 128;
+                    const int ch0 = ((c & 63) >> 3);
+                    *reinterpret_cast<uint4*>(atom + (((ch0) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                    *reinterpret_cast<uint4*>(atom + (((ch0 + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                }
+                l += sum;
+                fence_async_smem();
                 tc_fence_before();
-                mbar_arrive(o_empty);
+                mbar_arrive(&p_full[t]);
             }
-            alpha_prev = alpha;
-        }
-        wait_bar(o_full, (nkv - 1) & 1);
-        tc_fence_after();
+            wait_bar(&pv_done[t], (nkv - 1) & 1);
+            tc_fence_after();
+            const int qi = qp * 2 * BQ + t * BQ + r;
+            float o[HD];
 #pragma unroll
-        for (int c = 0; c < HD; c += 16) {
-            float v[16];
-            tmem_ld16(tmem + lane_off + 256 + c, v);
+            for (int c = 0; c < HD; c += 16) tmem_ld16(o_addr + c, o + c);
+            if (qi < a.q_len) {
+                const float inv = 1.f / l;
+                __nv_bfloat16* op = a.out + static_cast<long long>(q_row0 + t * BQ + r) * a.ld_out + a.out_col0 + head * HD;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * alpha_prev + v[i];
-        }
-        const int qi = qb * BQ + r;
-        if (qi < a.q_len) {
-            const float inv = 1.f / l;
-            __nv_bfloat16* op = a.out + static_cast<long long>(q_row0 + r) * a.ld_out + a.out_col0 + head * HD;
-#pragma unroll
-            for (int c = 0; c < HD; c += 8) {
-                uint4 w;
-                w.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
-                w.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
-                w.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
-                w.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
-                *reinterpret_cast<uint4*>(op + c) = w;
+                for (int c = 0; c < HD; c += 8) {
+                    uint4 w;
+                    w.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
+                    w.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
+                    w.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
+                    w.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
+                    *reinterpret_cast<uint4*>(op + c) = w;
+                }
             }
         }
     }
@@ -306,13 +330,13 @@ AttnPlan plan_attention(const __nv_bfloat16* q, long long q_rows_total, long lon
 
 void run_attention(const AttnPlan& p, cudaStream_t st) {
     static bool attr = false;
-    const size_t smem = 9 * TILE_BYTES + 1024 + 256;
+    const size_t smem = 10 * TILE_BYTES + 1024 + 256;
     if (!attr) {
         SDX_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;
     }
-    dim3 grid((p.a.q_len + BQ - 1) / BQ, p.heads, p.images);
-    attn_kernel<<<grid, 192, smem, st>>>(p.tq, p.tkv, p.a);
+    dim3 grid((p.a.q_len + 2 * BQ - 1) / (2 * BQ), p.heads, p.images);
+    attn_kernel<<<grid, 320, smem, st>>>(p.tq, p.tkv, p.a);
     SDX_LAUNCH_CHECK();
 }
 

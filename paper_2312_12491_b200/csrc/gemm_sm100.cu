@@ -1,11 +1,11 @@
 // tcgen05 / TMA GEMM + implicit-GEMM conv3x3 (see gemm_sm100.cuh).
 //
-// One 128 x BN output tile per CTA, 6 warps:
+// Persistent CTAs (one per SM) walking 128 x BN output tiles, 6 warps:
 //   warp 0      TMA producer (one elected lane): A and B K-slices (64 wide,
 //               128-byte swizzle) into a STAGES-deep smem ring (full/empty mbarriers)
 //   warp 1      TMEM allocation + MMA issuer (one lane): 4 x tcgen05.mma
 //               (M=128, N=BN, K=16) per stage, tcgen05.commit frees the stage
-//   warps 2..5  epilogue: tcgen05.ld 32 lanes x 16 columns, bias / per-image
+//   warps 2..9  epilogue (two per TMEM lane quadrant): tcgen05.ld 32 lanes x 16 columns, bias / per-image
 //               bias / activation / residual in fp32, bf16 or fp32 stores
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -28,6 +28,8 @@ namespace {
 struct GemmArgs {
     int M, N, K, K1, amode;
     int Ho, Wo, Cin, stride, Wt, Ht, Nt;
+    int splits;   // split-K factor (> 1: raw fp32 partials to ws, epilogue in splitk_reduce)
+    float* ws;    // [splits][M][N]
     GemmEpilogue epi;
 };
 
@@ -133,25 +135,28 @@ __device__ __forceinline__ void epilogue16(const GemmEpilogue& e, int N, long lo
     }
 }
 
+// Persistent: grid = min(tiles, SMs); tiles in (m, n) order with n fastest so
+// consecutive tiles share the A block in L2.  Two TMEM accumulators let the
+// epilogue of tile i overlap the MMAs of tile i+1.
 template <int BN, int STAGES, int AMODE>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
                    const __grid_constant__ CUtensorMap tb, const GemmArgs g) {
     constexpr int BM = 128, BK = 64;
     constexpr uint32_t A_BYTES = BM * BK * 2;
     constexpr uint32_t B_BYTES = BN * BK * 2;
-    constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+    constexpr uint32_t TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
 
-    const int n_tile = blockIdx.x;
-    const int m_tile = blockIdx.y;
-    const int m0 = m_tile * BM;
-    const int n0 = n_tile * BN;
     int m_eff = g.M;
     if (g.epi.rows_dev) {
         const long long lim = static_cast<long long>(*g.epi.rows_dev) * g.epi.rows_per_unit;
         if (lim < m_eff) m_eff = static_cast<int>(lim);
     }
-    if (m0 >= m_eff) return;  // device-decided batch: rows past the live count do no work
+    const int n_tiles = (g.N + BN - 1) / BN;
+    const int m_tiles = (m_eff + BM - 1) / BM;  // device-decided batch: only live rows' tiles
+    const int splits = g.splits;
+    const int total = m_tiles * n_tiles * splits;  // work units: (tile, K split)
+    if (static_cast<int>(blockIdx.x) >= total) return;
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -159,8 +164,9 @@ __global__ void __launch_bounds__(192, 1)
     uint8_t* sB = smem + STAGES * A_BYTES;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* done = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = empty + STAGES;   // [2]
+    uint64_t* tempty = tfull + 2;       // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -174,7 +180,10 @@ __global__ void __launch_bounds__(192, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 8);  // one arrival per epilogue warp
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -185,78 +194,212 @@ __global__ void __launch_bounds__(192, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            // conv tile origin in output space
-            int cn0 = 0, cy0 = 0, cx0 = 0;
-            if (AMODE == kAConv) {
-                const int hw = g.Ho * g.Wo;
-                cn0 = m0 / hw;
-                const int rem = m0 - cn0 * hw;
-                cy0 = rem / g.Wo;
-                cx0 = rem - cy0 * g.Wo;
-            }
             const int cblocks = AMODE == kAConv ? g.Cin / BK : 1;
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                wait_bounded(&empty[s], ph ^ 1);
-                mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                uint8_t* dA = sA + s * A_BYTES;
-                if (AMODE == kAMatrix) {
-                    tma_load_2d(dA, &ta, &full[s], kb * BK, m0);
-                } else if (AMODE == kAConcat) {
-                    const int k1b = g.K1 / BK;
-                    if (kb < k1b) tma_load_2d(dA, &ta, &full[s], kb * BK, m0);
-                    else tma_load_2d(dA, &ta2, &full[s], (kb - k1b) * BK, m0);
-                } else {
-                    const int tap = kb / cblocks;
-                    const int cb = kb - tap * cblocks;
-                    const int dy = tap / 3, dx = tap - dy * 3;
-                    tma_load_4d(dA, &ta, &full[s], cb * BK, cx0 * g.stride + dx - 1, cy0 * g.stride + dy - 1, cn0);
+            uint32_t it = 0;
+            for (int u = blockIdx.x; u < total; u += gridDim.x) {
+                const int t = u / splits, sp = u - t * splits;
+                const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
+                const int m0 = (t / n_tiles) * BM;
+                const int n0 = (t % n_tiles) * BN;
+                int cn0 = 0, cy0 = 0, cx0 = 0;
+                if (AMODE == kAConv) {
+                    const int hw = g.Ho * g.Wo;
+                    cn0 = m0 / hw;
+                    const int rem = m0 - cn0 * hw;
+                    cy0 = rem / g.Wo;
+                    cx0 = rem - cy0 * g.Wo;
                 }
-                tma_load_2d(sB + s * B_BYTES, &tb, &full[s], kb * BK, n0);
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    wait_bounded(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                    uint8_t* dA = sA + s * A_BYTES;
+                    if (AMODE == kAMatrix) {
+                        tma_load_2d(dA, &ta, &full[s], kb * BK, m0);
+                    } else if (AMODE == kAConcat) {
+                        const int k1b = g.K1 / BK;
+                        if (kb < k1b) tma_load_2d(dA, &ta, &full[s], kb * BK, m0);
+                        else tma_load_2d(dA, &ta2, &full[s], (kb - k1b) * BK, m0);
+                    } else {
+                        const int tap = kb / cblocks;
+                        const int cb = kb - tap * cblocks;
+                        const int dy = tap / 3, dx = tap - dy * 3;
+                        tma_load_4d(dA, &ta, &full[s], cb * BK, cx0 * g.stride + dx - 1, cy0 * g.stride + dy - 1, cn0);
+                    }
+                    tma_load_2d(sB + s * B_BYTES, &tb, &full[s], kb * BK, n0);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
-            for (int kb = 0; kb < nk; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                wait_bounded(&full[s], ph);
+            uint32_t it = 0, lt = 0;
+            for (int u = blockIdx.x; u < total; u += gridDim.x, ++lt) {
+                const int sp = u % splits;
+                const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
+                const uint32_t acc = lt & 1;
+                wait_bounded(&tempty[acc], ((lt >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint64_t da = desc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
-                const uint64_t db = desc_kmajor_sw128(smem_u32(sB + s * B_BYTES));
+                const uint32_t dtm = tmem + acc * BN;
+                for (int kb = kb0; kb < kb1; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    wait_bounded(&full[s], ph);
+                    tc_fence_after();
+                    const uint64_t da = desc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
+                    const uint64_t db = desc_kmajor_sw128(smem_u32(sB + s * B_BYTES));
 #pragma unroll
-                for (int k = 0; k < BK / 16; ++k)  // +32 bytes per K=16 step inside the swizzle atom
-                    umma_f16(tmem, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-                umma_commit(&empty[s]);
+                    for (int k = 0; k < BK / 16; ++k)  // +32 bytes per K=16 step inside the swizzle atom
+                        umma_f16(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&tfull[acc]);
             }
-            umma_commit(done);
         }
         __syncwarp();
     } else {
-        // epilogue warps 2..5 -> TMEM lane quadrants 2,3,0,1
+        // epilogue warps 2..5 -> TMEM lane quadrants 2,3,0,1.  Per 32-column chunk:
+        // phase 1: tcgen05.ld 32 fp32 of the thread's row, scale + bias + per-image
+        // bias, staged in this warp's smem slab (row pitch 144 B);  phase 2: the warp
+        // re-reads the slab so 4 lanes cover one row's 32 columns, adds the residual,
+        // applies the activation and writes 16-byte coalesced stores.
         const int q = warp & 3;
-        wait_bounded(done, 0);
-        tc_fence_after();
-        const int row = m0 + q * 32 + lane;
-        const bool row_ok = row < m_eff;
-        const GemmEpilogue& e = g.epi;
-        const float* bimg = nullptr;
-        long long orow = row;  // destination row (scatter by image when out_img_map is set)
-        if (row_ok) {
-            const long long im = static_cast<long long>(row) / e.rows_per_img;
-            if (e.bias_img)
-                bimg = e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : g.N);
-            if (e.out_img_map) orow = static_cast<long long>(e.out_img_map[im]) * e.rows_per_img + (row - im * e.rows_per_img);
+        const int half = (warp - 2) >> 2;  // two warps per lane quadrant split the 32-column chunks
+        GemmEpilogue e = g.epi;
+        if (splits > 1) {  // raw partial sums; splitk_reduce applies the real epilogue
+            e = GemmEpilogue{};
+            e.out_f32 = 1;
+            e.ld_out = g.N;
         }
+        float* slab = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16) + (warp - 2) * (32 * 32);
+        uint32_t lt = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x, ++lt) {
+            const int t = u / splits;
+            if (splits > 1) e.out = g.ws + static_cast<long long>(u % splits) * g.M * g.N;
+            const uint32_t acc = lt & 1;
+            const int m0 = (t / n_tiles) * BM;
+            const int n0 = (t % n_tiles) * BN;
+            wait_bounded(&tfull[acc], (lt >> 1) & 1);
+            tc_fence_after();
+            const int row = m0 + q * 32 + lane;
+            const float* bimg = nullptr;
+            if (e.bias_img && row < m_eff) {
+                const long long im = static_cast<long long>(row) / e.rows_per_img;
+                bimg = e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : g.N);
+            }
+            const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 16) {
-            float v[16];
-            tmem_ld16(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-            const int col0 = n0 + c;
-            if (!row_ok || col0 >= g.N) continue;
-            epilogue16(e, g.N, row, orow, col0, bimg, v);
+            for (int c = half * 32; c < BN; c += 64) {
+                uint32_t r[32];
+                tmem_ld32_nowait(tbase + c, r);
+                tmem_wait_ld();
+                const int col0 = n0 + c;
+                if (col0 >= g.N) continue;  // warp-uniform
+                const bool vec_ok = col0 + 32 <= g.N;
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * e.scale;
+                if (e.bias) {
+                    if (vec_ok) {
+#pragma unroll
+                        for (int i = 0; i < 32; i += 4) {
+                            const float4 b = *reinterpret_cast<const float4*>(e.bias + col0 + i);
+                            v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+                        }
+                    } else {
+                        for (int i = 0; i < 32; ++i)
+                            if (col0 + i < g.N) v[i] += e.bias[col0 + i];
+                    }
+                }
+                if (bimg) {
+                    for (int i = 0; i < 32; ++i)
+                        if (col0 + i < g.N) v[i] += bimg[col0 + i];
+                }
+                if (e.geglu) {  // interleaved [16 value | 16 gate] columns -> 16 outputs
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = v[i] * 0.5f * v[16 + i] * (1.f + erff(v[16 + i] * 0.70710678118654752f));
+                }
+                __syncwarp();
+                // slab row = 8 x 16-byte chunks, chunk index XOR (row % 8): conflict-free both ways
+                float* srow = slab + lane * 32;
+#pragma unroll
+                for (int i = 0; i < 32; i += 4)
+                    *reinterpret_cast<float4*>(srow + (((i >> 2) ^ (lane & 7)) << 2)) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                __syncwarp();
+                // phase 2: lane -> (row, 8 columns); 4 lanes per row (2 for GEGLU's 16 outputs)
+                const int lpr_shift = e.geglu ? 1 : 2;
+                const int pc = (lane & ((1 << lpr_shift) - 1)) * 8;
+                const int nout = e.geglu ? g.N / 2 : g.N;
+                const int ocol0 = e.geglu ? col0 / 2 : col0;
+#pragma unroll 1
+                for (int rr = 0; rr < 32; rr += (32 >> lpr_shift)) {
+                    const int lr = rr + (lane >> lpr_shift);
+                    const int grow = m0 + q * 32 + lr;
+                    if (grow >= m_eff) continue;
+                    const int gcol = ocol0 + pc;
+                    if (gcol >= nout) continue;
+                    const float* sr = slab + lr * 32;
+                    float w8[8];
+                    const float4 a0 = *reinterpret_cast<const float4*>(sr + ((((pc >> 2)) ^ (lr & 7)) << 2));
+                    const float4 a1 = *reinterpret_cast<const float4*>(sr + ((((pc >> 2) + 1) ^ (lr & 7)) << 2));
+                    w8[0] = a0.x; w8[1] = a0.y; w8[2] = a0.z; w8[3] = a0.w;
+                    w8[4] = a1.x; w8[5] = a1.y; w8[6] = a1.z; w8[7] = a1.w;
+                    const bool full8 = gcol + 8 <= nout;
+                    if (!e.act_after_residual) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) w8[i] = act_fn(w8[i], e.act);
+                    }
+                    if (e.residual) {
+                        const __nv_bfloat16* rp = e.residual + static_cast<long long>(grow) * e.ld_res + gcol;
+                        if (full8) {
+                            const uint4 rv = *reinterpret_cast<const uint4*>(rp);
+                            const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) w8[i] += __bfloat162float(rb[i]);
+                        } else {
+                            for (int i = 0; i < 8 && gcol + i < nout; ++i) w8[i] += __bfloat162float(rp[i]);
+                        }
+                    }
+                    if (e.act_after_residual) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) w8[i] = act_fn(w8[i], e.act);
+                    }
+                    long long orow = grow;
+                    if (e.out_img_map) {
+                        const long long im = static_cast<long long>(grow) / e.rows_per_img;
+                        orow = static_cast<long long>(e.out_img_map[im]) * e.rows_per_img + (grow - im * e.rows_per_img);
+                    }
+                    if (e.out_f32 == 1) {
+                        float* op = reinterpret_cast<float*>(e.out) + orow * e.ld_out + gcol;
+                        if (full8) {
+                            *reinterpret_cast<float4*>(op) = make_float4(w8[0], w8[1], w8[2], w8[3]);
+                            *reinterpret_cast<float4*>(op + 4) = make_float4(w8[4], w8[5], w8[6], w8[7]);
+                        } else {
+                            for (int i = 0; i < 8 && gcol + i < nout; ++i) op[i] = w8[i];
+                        }
+                    } else if (e.out_f32 == 2) {
+                        uint8_t* op = reinterpret_cast<uint8_t*>(e.out) + orow * e.ld_out + gcol;
+                        for (int i = 0; i < 8 && gcol + i < nout; ++i)
+                            op[i] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(w8[i], 0.f), 1.f) * 255.f));
+                    } else {
+                        __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + orow * e.ld_out + gcol;
+                        if (full8) {
+                            uint4 o;
+                            o.x = pack_bf16(w8[0], w8[1]);
+                            o.y = pack_bf16(w8[2], w8[3]);
+                            o.z = pack_bf16(w8[4], w8[5]);
+                            o.w = pack_bf16(w8[6], w8[7]);
+                            *reinterpret_cast<uint4*>(op) = o;
+                        } else {
+                            for (int i = 0; i < 8 && gcol + i < nout; ++i) op[i] = __float2bfloat16(w8[i]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
         }
     }
     tc_fence_before();
@@ -264,6 +407,69 @@ __global__ void __launch_bounds__(192, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
+    }
+}
+
+// Split-K finish: sum the fp32 partials and apply the full epilogue, 8 columns
+// per thread, coalesced.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, GemmEpilogue e) {
+    int m_eff = M;
+    if (e.rows_dev) {
+        const long long lim = static_cast<long long>(*e.rows_dev) * e.rows_per_unit;
+        if (lim < m_eff) m_eff = static_cast<int>(lim);
+    }
+    const int nv = (N + 7) / 8;
+    const long long total = static_cast<long long>(m_eff) * nv;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const int row = static_cast<int>(idx / nv);
+        const int col = static_cast<int>(idx % nv) * 8;
+        const int cnt = N - col < 8 ? N - col : 8;
+        float w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int sp = 0; sp < splits; ++sp) {
+            const float* p = ws + (static_cast<long long>(sp) * M + row) * N + col;
+            if (cnt == 8 && (N % 4) == 0) {
+                const float4 a = *reinterpret_cast<const float4*>(p);
+                const float4 b = *reinterpret_cast<const float4*>(p + 4);
+                w[0] += a.x; w[1] += a.y; w[2] += a.z; w[3] += a.w;
+                w[4] += b.x; w[5] += b.y; w[6] += b.z; w[7] += b.w;
+            } else {
+                for (int i = 0; i < cnt; ++i) w[i] += p[i];
+            }
+        }
+        const long long im = row / e.rows_per_img;
+        const float* bimg = e.bias_img ? e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : N)
+                                       : nullptr;
+        for (int i = 0; i < cnt; ++i) {
+            float x = w[i] * e.scale;
+            if (e.bias) x += e.bias[col + i];
+            if (bimg) x += bimg[col + i];
+            if (!e.act_after_residual) x = act_fn(x, e.act);
+            if (e.residual) x += __bfloat162float(e.residual[static_cast<long long>(row) * e.ld_res + col + i]);
+            if (e.act_after_residual) x = act_fn(x, e.act);
+            w[i] = x;
+        }
+        long long orow = row;
+        if (e.out_img_map) orow = static_cast<long long>(e.out_img_map[im]) * e.rows_per_img + (row - im * e.rows_per_img);
+        if (e.out_f32 == 1) {
+            float* op = reinterpret_cast<float*>(e.out) + orow * e.ld_out + col;
+            for (int i = 0; i < cnt; ++i) op[i] = w[i];
+        } else if (e.out_f32 == 2) {
+            uint8_t* op = reinterpret_cast<uint8_t*>(e.out) + orow * e.ld_out + col;
+            for (int i = 0; i < cnt; ++i) op[i] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(w[i], 0.f), 1.f) * 255.f));
+        } else {
+            __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + orow * e.ld_out + col;
+            if (cnt == 8 && (e.ld_out % 8) == 0) {
+                uint4 o;
+                o.x = pack_bf16(w[0], w[1]);
+                o.y = pack_bf16(w[2], w[3]);
+                o.z = pack_bf16(w[4], w[5]);
+                o.w = pack_bf16(w[6], w[7]);
+                *reinterpret_cast<uint4*>(op) = o;
+            } else {
+                for (int i = 0; i < cnt; ++i) op[i] = __float2bfloat16(w[i]);
+            }
+        }
     }
 }
 
@@ -305,20 +511,34 @@ void encode_2d(CUtensorMap* m, const void* ptr, long long rows, long long cols, 
     encode(m, ptr, 2, dims, strides, box, es);
 }
 
+// Largest UMMA N (multiple of 32, <= 256) that minimises padded columns.
 int pick_bn(int N) {
     if (N <= 64) return 64;
-    if (N % 256 == 0 || N > 640) return 256;
-    return 128;
+    static const int cand[] = {256, 224, 192, 160, 128, 96, 64};
+    int best = 64;
+    long long best_cost = -1;
+    for (int bn : cand) {
+        const long long tiles = (N + bn - 1) / bn;
+        const long long waste = tiles * bn - N;
+        // cost: padded work plus a per-tile overhead (A re-read per N tile)
+        const long long cost = waste * 4 + tiles * 24;
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = bn;
+        }
+    }
+    return best;
 }
 
 template <int BN>
 constexpr int stages_for() {
-    return BN == 256 ? 4 : 6;
+    return BN >= 192 ? 4 : (BN >= 128 ? 5 : 6);
 }
 
 template <int BN>
 size_t smem_for() {
-    return static_cast<size_t>(stages_for<BN>()) * (128 * 64 * 2 + BN * 64 * 2) + 1024 + 256;
+    // stages + barriers (256 B) + 8 epilogue slabs of 32 x 32 fp32
+    return static_cast<size_t>(stages_for<BN>()) * (128 * 64 * 2 + BN * 64 * 2) + 1024 + 256 + 8 * 32 * 32 * 4;
 }
 
 template <int BN, int AMODE>
@@ -345,21 +565,53 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
     g.Ht = p.Ht;
     g.Nt = p.Nt;
     g.epi = p.epi;
-    dim3 grid((p.N + BN - 1) / BN, (p.M + 127) / 128);
-    k<<<grid, 192, smem, st>>>(p.ta, p.ta2, p.tb, g);
+    g.splits = p.splits;
+    g.ws = p.ws;
+    const int units = ((p.N + BN - 1) / BN) * ((p.M + 127) / 128) * p.splits;
+    dim3 grid(units < kSmCount ? units : kSmCount);
+    k<<<grid, 320, smem, st>>>(p.ta, p.ta2, p.tb, g);
     SDX_LAUNCH_CHECK();
+    if (p.splits > 1) {
+        const long long work = static_cast<long long>(p.M) * ((p.N + 7) / 8);
+        long long blocks = (work + 255) / 256;
+        if (blocks > 4LL * kSmCount) blocks = 4LL * kSmCount;
+        splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(p.ws, p.splits, p.M, p.N, p.epi);
+        SDX_LAUNCH_CHECK();
+    }
 }
 
 template <int AMODE>
 void launch_mode(const GemmPlan& p, cudaStream_t st) {
     switch (p.bn) {
         case 64: launch_t<64, AMODE>(p, st); break;
-        case 256: launch_t<256, AMODE>(p, st); break;
-        default: launch_t<128, AMODE>(p, st); break;
+        case 96: launch_t<96, AMODE>(p, st); break;
+        case 128: launch_t<128, AMODE>(p, st); break;
+        case 160: launch_t<160, AMODE>(p, st); break;
+        case 192: launch_t<192, AMODE>(p, st); break;
+        case 224: launch_t<224, AMODE>(p, st); break;
+        default: launch_t<256, AMODE>(p, st); break;
     }
 }
 
 }  // namespace
+
+// Split-K when the output has too few tiles to fill the SMs and K is long.
+void choose_splits(GemmPlan& p) {
+    const int tiles = ((p.N + p.bn - 1) / p.bn) * ((p.M + 127) / 128);
+    const int nk = p.K / 64;
+    int splits = 1;
+    if (tiles < 100 && nk >= 8 && !p.epi.geglu) {
+        splits = kSmCount / tiles;
+        if (splits > nk / 4) splits = nk / 4;
+        if (splits < 1) splits = 1;
+    }
+    p.splits = splits;
+    if (splits > 1) {
+        float* ws = dev_alloc<float>(static_cast<size_t>(splits) * p.M * p.N);
+        p.ws = ws;
+        p.ws_owner = std::shared_ptr<void>(ws, [](void* q) { cudaFree(q); });
+    }
+}
 
 GemmPlan plan_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
                    const GemmEpilogue& epi) {
@@ -376,6 +628,7 @@ GemmPlan plan_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B
     p.epi = epi;
     if (p.epi.ld_out == 0) p.epi.ld_out = N;
     if (p.epi.residual && p.epi.ld_res == 0) p.epi.ld_res = N;
+    choose_splits(p);
     p.valid = true;
     return p;
 }
@@ -396,6 +649,7 @@ GemmPlan plan_gemm_concat(const __nv_bfloat16* A1, long long lda1, int K1, const
     p.epi = epi;
     if (p.epi.ld_out == 0) p.epi.ld_out = N;
     if (p.epi.residual && p.epi.ld_res == 0) p.epi.ld_res = N;
+    choose_splits(p);
     p.valid = true;
     return p;
 }
@@ -437,6 +691,7 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
     p.epi = epi;
     if (p.epi.ld_out == 0) p.epi.ld_out = Cout;
     if (p.epi.residual && p.epi.ld_res == 0) p.epi.ld_res = Cout;
+    choose_splits(p);
     p.valid = true;
     return p;
 }

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
 
 namespace sdx {
 
@@ -34,6 +35,7 @@ struct GemmEpilogue {
     long long ld_out = 0;
     int out_f32 = 0;                      // 0 bf16, 1 fp32, 2 u8 (round(255 * clamp(v, 0, 1)))
     int act_after_residual = 0;           // act(acc + bias + residual) instead of act(acc + bias) + residual
+    int geglu = 0;                        // B rows interleaved [16 value | 16 gate]: out[:, j] = a_j * gelu(g_j), N/2 cols
     const int* out_img_map = nullptr;     // image -> destination image block of rows_per_img rows (scatter)
     const int* rows_dev = nullptr;        // device row-unit count (skip tiles past *rows_dev * rows_per_unit)
     long long rows_per_unit = 0;
@@ -48,6 +50,9 @@ struct GemmPlan {
     // conv geometry (amode == kAConv)
     int H = 0, W = 0, Cin = 0, Ho = 0, Wo = 0, stride = 1, Wt = 0, Ht = 0, Nt = 0;
     GemmEpilogue epi;
+    int splits = 1;                     // split-K factor (chosen when tiles cannot fill the SMs)
+    float* ws = nullptr;                // split-K fp32 partials
+    std::shared_ptr<void> ws_owner;     // frees ws with the last copy of the plan
     bool valid = false;
 };
 

@@ -84,6 +84,37 @@ __global__ void gn_stats_kernel(GnPlan p) {
         out[0] = a;
         out[1] = b;
     }
+    // the last chunk of this image to finish reduces all chunks: one warp per group,
+    // fp64 partial sums in a fixed order (deterministic), mean / rstd for apply
+    __shared__ unsigned int last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&p.counter[img], 1u) == static_cast<unsigned>(p.chunks - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int g = warp; g < p.groups; g += nw) {
+        double a = 0.0, b = 0.0;
+        for (int k = lane; k < p.chunks; k += 32) {
+            const float* pr = p.partial + ((static_cast<long long>(img) * p.chunks + k) * p.groups + g) * 2;
+            a += __ldcg(pr);
+            b += __ldcg(pr + 1);
+        }
+        for (int off = 16; off; off >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, off);
+            b += __shfl_xor_sync(0xffffffffu, b, off);
+        }
+        if (lane == 0) {
+            const double n = static_cast<double>(Ct / p.groups) * p.HW;
+            const double mean = a / n;
+            double var = b / n - mean * mean;
+            if (var < 0) var = 0;
+            p.stats[(img * p.groups + g) * 2] = static_cast<float>(mean);
+            p.stats[(img * p.groups + g) * 2 + 1] = static_cast<float>(1.0 / sqrt(var + p.eps));
+        }
+    }
+    if (threadIdx.x == 0) p.counter[img] = 0;
 }
 
 __global__ void gn_apply_kernel(GnPlan p) {
@@ -93,18 +124,8 @@ __global__ void gn_apply_kernel(GnPlan p) {
     const int Ct = p.C1 + p.C2;
     const int cg = Ct / p.groups;
     for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
-        double a = 0.0, b = 0.0;
-        for (int k = 0; k < p.chunks; ++k) {
-            const float* pr = p.partial + ((static_cast<long long>(img) * p.chunks + k) * p.groups + g) * 2;
-            a += pr[0];
-            b += pr[1];
-        }
-        const double n = static_cast<double>(cg) * p.HW;
-        const double mean = a / n;
-        double var = b / n - mean * mean;
-        if (var < 0) var = 0;
-        mean_s[g] = static_cast<float>(mean);
-        rstd_s[g] = static_cast<float>(1.0 / sqrt(var + p.eps));
+        mean_s[g] = p.stats[(img * p.groups + g) * 2];
+        rstd_s[g] = p.stats[(img * p.groups + g) * 2 + 1];
     }
     __syncthreads();
     const int noct = Ct / 8;
@@ -348,11 +369,16 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
     if (chunks > HW / 16) chunks = HW / 16 > 0 ? HW / 16 : 1;
     p.chunks = chunks;
     p.partial = dev_alloc<float>(static_cast<size_t>(imgs) * chunks * p.groups * 2);
+    p.stats = dev_alloc<float>(static_cast<size_t>(imgs) * p.groups * 2);
+    p.counter = dev_alloc<unsigned int>(static_cast<size_t>(imgs));
+    SDX_CUDA(cudaMemset(p.counter, 0, sizeof(unsigned int) * imgs));
     return p;
 }
 
 void free_groupnorm(GnPlan& p) {
     dev_free(p.partial);
+    dev_free(p.stats);
+    dev_free(p.counter);
     p.partial = nullptr;
 }
 
@@ -429,6 +455,19 @@ void fill_const_f32(float* p, long long n, float v, cudaStream_t st) {
     fill_const_kernel<<<grid_for(n, 256), 256, 0, st>>>(p, n, v);
     SDX_LAUNCH_CHECK();
 }
+__global__ void interleave_geglu_kernel(const bf16* w, const float* b, int H, int K, bf16* wout, float* bout) {
+    const int r = blockIdx.x;  // destination row
+    const int blk = r >> 5, wi = r & 31;
+    const int src = wi < 16 ? blk * 16 + wi : H + blk * 16 + (wi - 16);
+    for (int k = threadIdx.x; k < K; k += blockDim.x) wout[static_cast<long long>(r) * K + k] = w[static_cast<long long>(src) * K + k];
+    if (threadIdx.x == 0) bout[r] = b[src];
+}
+
+void run_interleave_geglu(const bf16* w, const float* b, int H, int K, bf16* wout, float* bout, cudaStream_t st) {
+    interleave_geglu_kernel<<<2 * H, 128, 0, st>>>(w, b, H, K, wout, bout);
+    SDX_LAUNCH_CHECK();
+}
+
 void run_tanh_clamp(const float* in, float* out, long long n, cudaStream_t st) {
     tanh_clamp_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
     SDX_LAUNCH_CHECK();

@@ -21,6 +21,8 @@ struct GnPlan {
     int silu;
     bf16* out;
     float* partial;  // [imgs][chunks][groups][2]
+    float* stats;    // [imgs][groups][2] mean, rstd (written by the last stats block per image)
+    unsigned int* counter;  // [imgs] stats blocks finished
     int chunks;
     int imgs;
     const int* rows_dev;
@@ -57,6 +59,10 @@ void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStre
 void fill_normal_bf16(bf16* p, long long n, float std, uint64_t seed, cudaStream_t st);
 void fill_normal_f32(float* p, long long n, float std, uint64_t seed, cudaStream_t st);
 void fill_const_f32(float* p, long long n, float v, cudaStream_t st);
+
+// Reorders a GEGLU projection ([2H][K] weights, [2H] bias: value rows then gate
+// rows) into 16-row blocks [value 16j.. | gate 16j..] for the fused GEMM epilogue.
+void run_interleave_geglu(const bf16* w, const float* b, int H, int K, bf16* wout, float* bout, cudaStream_t st);
 
 // elementwise: TAESD decoder input clamp  y = tanh(x / 3) * 3  (fp32 -> fp32)
 void run_tanh_clamp(const float* in, float* out, long long n, cudaStream_t st);

@@ -198,12 +198,23 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
     // GEGLU feed-forward
     bf16* n3 = act(M * C);
     layernorm(h3, n3, nm + ".ln3");
-    bf16* ff = act(M * 8 * C);
-    gemm("linear", n3, C, wbf(nm + ".ff1.w", {8 * C, C}, wstd), 8 * C, wf32(nm + ".ff1.b", {8 * C}, 0.02f, 0.f), nullptr, ff);
     bf16* u = act(M * 4 * C);
     {
-        const int Mi = static_cast<int>(M);
-        ops_.push_back(Op{"geglu", [=](cudaStream_t st) { run_geglu(ff, Mi, 4 * C, u, rows, HW, st); }});
+        // FF1 with GEGLU fused in the epilogue: weights / bias permuted once into
+        // [16 value | 16 gate] row blocks (the registered parameter keeps the plain layout)
+        bf16* w1 = wbf(nm + ".ff1.w", {8 * C, C}, wstd);
+        float* b1 = wf32(nm + ".ff1.b", {8 * C}, 0.02f, 0.f);
+        bf16* w1i = act(8LL * C * C);
+        float* b1i = actf(8LL * C);
+        run_interleave_geglu(w1, b1, 4 * C, C, w1i, b1i, nullptr);
+        GemmEpilogue e;
+        e.bias = b1i;
+        e.geglu = 1;
+        e.out = u;
+        e.ld_out = 4 * C;
+        e.rows_dev = rows;
+        e.rows_per_unit = HW;
+        gemm_op("linear_geglu", plan_gemm(n3, C, w1i, C, static_cast<int>(M), 8 * C, C, e));
     }
     bf16* h4 = act(M * C);
     gemm("linear", u, 4 * C, wbf(nm + ".ff2.w", {C, 4 * C}, 1.f / std::sqrt(4.f * C)), C,

@@ -1,0 +1,21 @@
+"""Runs the device UNet forward a few times (for ncu launch lists / captures)."""
+import ctypes as C
+import sys
+
+sys.path.insert(0, ".")
+from paper_2312_12491_b200 import _lib  # noqa: E402
+
+L = _lib.lib
+vp = C.c_void_p
+L.sdx_unet_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_uint64, C.c_int, C.POINTER(vp)]
+L.sdx_unet_forward.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), vp, vp]
+rows = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+taus = (C.c_int * 4)(999, 749, 499, 249)
+h = vp()
+assert L.sdx_unet_create(rows, taus, 4, 1234, 0, C.byref(h)) == 0
+steps = (C.c_int * rows)(*[i % 4 for i in range(rows)])
+prompts = (C.c_int * rows)(*[0] * rows)
+for _ in range(iters):
+    assert L.sdx_unet_forward(h, None, rows, steps, prompts, None, None) == 0
+print("ok")
