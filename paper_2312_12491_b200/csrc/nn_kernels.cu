@@ -141,11 +141,16 @@ __global__ void gn_apply_kernel(GnPlan p) {
                                 : p.x2 + (static_cast<long long>(img) * p.HW + px) * p.C2 + (c - p.C1);
         float v[8];
         load8(src, v);
+        const int g0 = c / cg;
+        const int gb = (g0 + 1) * cg;  // first channel of the next group
+        const float4 ga = *reinterpret_cast<const float4*>(p.gamma + c), gb4 = *reinterpret_cast<const float4*>(p.gamma + c + 4);
+        const float4 ba = *reinterpret_cast<const float4*>(p.beta + c), bb4 = *reinterpret_cast<const float4*>(p.beta + c + 4);
+        const float gam[8] = {ga.x, ga.y, ga.z, ga.w, gb4.x, gb4.y, gb4.z, gb4.w};
+        const float bet[8] = {ba.x, ba.y, ba.z, ba.w, bb4.x, bb4.y, bb4.z, bb4.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int ch = c + i;
-            const int g = ch / cg;
-            float y = (v[i] - mean_s[g]) * rstd_s[g] * p.gamma[ch] + p.beta[ch];
+            const int g = (c + i) < gb ? g0 : g0 + 1;  // an octet spans at most two groups (cg >= 8)
+            float y = (v[i] - mean_s[g]) * rstd_s[g] * gam[i] + bet[i];
             v[i] = p.silu ? silu(y) : y;
         }
         store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v);
@@ -201,7 +206,14 @@ __global__ void layernorm_kernel(const bf16* __restrict__ x, int rows, int C, co
         if (o < noct) {
             float y[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) y[i] = (v[k][i] - mean) * rstd * gamma[o * 8 + i] + beta[o * 8 + i];
+            for (int i = 0; i < 8; i += 4) {
+                const float4 gm = *reinterpret_cast<const float4*>(gamma + o * 8 + i);
+                const float4 bt = *reinterpret_cast<const float4*>(beta + o * 8 + i);
+                y[i] = (v[k][i] - mean) * rstd * gm.x + bt.x;
+                y[i + 1] = (v[k][i + 1] - mean) * rstd * gm.y + bt.y;
+                y[i + 2] = (v[k][i + 2] - mean) * rstd * gm.z + bt.z;
+                y[i + 3] = (v[k][i + 3] - mean) * rstd * gm.w + bt.w;
+            }
             store8(orow + o * 8, y);
         }
     }
@@ -364,9 +376,13 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
     const int Ct = p.C1 + p.C2;
     if (Ct % 8 != 0 || Ct % p.groups != 0 || (p.C2 && p.C1 % 8 != 0))
         raise(SDX_INVALID_ARGUMENT, "groupnorm: channels must be multiples of 8 and 32");
-    int chunks = 2 * 148 / (imgs > 0 ? imgs : 1);
-    if (chunks < 4) chunks = 4;
-    if (chunks > HW / 16) chunks = HW / 16 > 0 ? HW / 16 : 1;
+    // ~4 pixels per thread per stats block: enough blocks to keep HBM busy
+    const int noct = Ct / 8;
+    const int threads = noct >= 256 ? noct : noct * (256 / noct);
+    const int per = threads / noct;
+    int chunks = HW / (per * 4);
+    if (chunks < 1) chunks = 1;
+    if (chunks > 1024) chunks = 1024;
     p.chunks = chunks;
     p.partial = dev_alloc<float>(static_cast<size_t>(imgs) * chunks * p.groups * 2);
     p.stats = dev_alloc<float>(static_cast<size_t>(imgs) * p.groups * 2);
@@ -390,7 +406,10 @@ void run_groupnorm(const GnPlan& p, cudaStream_t st) {
     const int per = threads / noct;
     gn_stats_kernel<<<g1, threads, static_cast<size_t>(per) * 2 * Ct * sizeof(float), st>>>(p);
     SDX_LAUNCH_CHECK();
-    gn_apply_kernel<<<g1, 256, 0, st>>>(p);
+    // apply: ~4 octets per thread
+    int ab = static_cast<int>((static_cast<long long>(p.HW) * noct + 1023) / 1024);
+    if (ab < 1) ab = 1;
+    gn_apply_kernel<<<dim3(ab, p.imgs), 256, 0, st>>>(p);
     SDX_LAUNCH_CHECK();
 }
 
