@@ -49,6 +49,8 @@ def parse():
     p.add_argument("--no-ssf", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--profile-window", action="store_true",
+                   help="cudaProfilerStart/Stop around the timed resident loop (ncu --profile-from-start off)")
     return p.parse_args()
 
 
@@ -201,9 +203,13 @@ def run_ours(args, dist: Dist):
     with Clocks(dev) as clk:
         p.sync()
         p.reset_timer()
+        if args.profile_window:
+            L.lib.sdx_profiler_start()
         for _ in range(args.steps):
             p.push_resident(copy_outputs=False)
         ms = p.device_time_ms()
+        if args.profile_window:
+            L.lib.sdx_profiler_stop()
         p.sync()
     stages = p.stage_times()
     ms_max = dist.max(ms)

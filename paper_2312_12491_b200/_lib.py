@@ -101,6 +101,8 @@ _sig = {
     "sdx_sample_gaussian": (C.c_int, [C.c_uint64, C.c_int64, D]),
     "sdx_build_noise_cache": (C.c_int, [C.c_uint64, C.c_int, C.c_int64, D]),
     "sdx_precompute_error": (C.c_char_p, []),
+    "sdx_profiler_start": (C.c_int, []),
+    "sdx_profiler_stop": (C.c_int, []),
     "sdx_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
     "sdx_host_free": (C.c_int, [C.c_void_p]),
 }

@@ -180,3 +180,11 @@ int sdx_memcpy_d2d(void* dst, const void* src, int64_t bytes) {
 }
 
 }  // extern "C"
+
+#include <cuda_profiler_api.h>
+
+extern "C" {
+// Bracket a region for `ncu --profile-from-start off` (bench.py --profile-window).
+int sdx_profiler_start(void) { return kguard([&] { SDX_CUDA(cudaProfilerStart()); }); }
+int sdx_profiler_stop(void) { return kguard([&] { SDX_CUDA(cudaProfilerStop()); }); }
+}
