@@ -63,6 +63,25 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return "\n".join(logs)
 
 
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "_bin", "test_dropin")
+
+
+def build_cpp_tests() -> str:
+    """The C++ drop-in test: reference test cases on include/stagger_b200/stagger/*.hpp,
+    checked against the C oracle (oracle/_build/liboracle.so)."""
+    oracle_dir = os.path.join(ROOT, "oracle")
+    deps = [CPP_TEST_SRC, LIB] + glob.glob(os.path.join(INCLUDE, "stagger_b200", "stagger", "*.hpp"))
+    if not _stale(CPP_TEST_BIN, deps):
+        return ""
+    os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(INCLUDE, "stagger_b200"), "-I", INCLUDE,
+           "-I", oracle_dir, CPP_TEST_SRC, "-o", CPP_TEST_BIN,
+           "-L", PKG, "-lstagger_b200", "-Wl,-rpath," + PKG,
+           "-L", os.path.join(oracle_dir, "_build"), "-loracle", "-Wl,-rpath," + os.path.join(oracle_dir, "_build")]
+    return _run(cmd)
+
+
 if __name__ == "__main__":
     out = build(verbose="-v" in sys.argv, force="-f" in sys.argv)
     if out.strip():
