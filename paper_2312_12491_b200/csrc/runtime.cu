@@ -531,6 +531,8 @@ Pipeline::~Pipeline() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
     if (copy_) cudaStreamSynchronize(copy_);
+    for (auto gexec : graphs_)
+        if (gexec) cudaGraphExecDestroy(gexec);
     taesd_.reset();
     unet_.reset();
     dev_free(lists_buf_);
@@ -561,7 +563,6 @@ void Pipeline::launch_iteration(int k, bool frame_present) {
     };
     mark(0);
     if (frame_present) {
-        SDX_CUDA(cudaStreamWaitEvent(stream_, h2d_[static_cast<size_t>(k)], 0));
         if (e.ssf_enabled) {
             SsfArgs a{};
             a.frames = frames;
@@ -634,6 +635,36 @@ void Pipeline::launch_iteration(int k, bool frame_present) {
                                 : static_cast<const void*>(dev_.emitted);
         SDX_CUDA(cudaMemcpyAsync(h_out_ + static_cast<size_t>(k) * S_ * out_bytes_, src, out_bytes_ * S_,
                                  cudaMemcpyDeviceToHost, stream_));
+    }
+}
+
+// One iteration on ring slot k: wait for the slot's H2D, run the iteration
+// (replaying its CUDA graph when graphs are enabled), mark completion.
+void Pipeline::run_iteration(int k, bool frame_present) {
+    if (frame_present) SDX_CUDA(cudaStreamWaitEvent(stream_, h2d_[static_cast<size_t>(k)], 0));
+    const bool use_graph = cfg_.graph && frame_present && !profile_;
+    if (!use_graph) {
+        launch_iteration(k, frame_present);
+    } else {
+        // one graph per (ring slot, output-copy variant): pointers differ per slot
+        const int key = k * 2 + ((!resident_ || copy_outputs_) ? 1 : 0);
+        if (graphs_.size() < static_cast<size_t>(2 * K_)) {
+            graphs_.assign(static_cast<size_t>(2 * K_), nullptr);
+            graph_launches_.assign(static_cast<size_t>(2 * K_), 0);
+        }
+        if (!graphs_[static_cast<size_t>(key)]) {
+            const long long before = launches_;
+            cudaGraph_t g = nullptr;
+            SDX_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+            launch_iteration(k, frame_present);
+            SDX_CUDA(cudaStreamEndCapture(stream_, &g));
+            SDX_CUDA(cudaGraphInstantiate(&graphs_[static_cast<size_t>(key)], g, 0));
+            SDX_CUDA(cudaGraphDestroy(g));
+            graph_launches_[static_cast<size_t>(key)] = launches_ - before;
+            launches_ = before;
+        }
+        SDX_CUDA(cudaGraphLaunch(graphs_[static_cast<size_t>(key)], stream_));
+        launches_ += graph_launches_[static_cast<size_t>(key)];
     }
     SDX_CUDA(cudaEventRecord(done_[static_cast<size_t>(k)], stream_));
 }
@@ -776,7 +807,7 @@ void Pipeline::push(const uint8_t* frames) {
         // resident mode: frames already in ring slot k (upload_resident)
         SDX_CUDA(cudaEventRecord(h2d_[static_cast<size_t>(k)], stream_));
     }
-    launch_iteration(k, true);
+    run_iteration(k, true);
     inflight_.push_back({k, true});
     iter_ += 1;
     drain_completed(false);
@@ -819,7 +850,7 @@ void Pipeline::finish() {
     for (int i = 0; i < rem; ++i) {
         const int k = static_cast<int>(iter_ % K_);
         while (static_cast<int>(inflight_.size()) >= K_) drain_completed(true);
-        launch_iteration(k, false);
+        run_iteration(k, false);
         inflight_.push_back({k, false});
         iter_ += 1;
     }

@@ -180,7 +180,10 @@ class Pipeline {
         std::string error;
     };
     void launch_iteration(int k, bool frame_present);
+    void run_iteration(int k, bool frame_present);
     void process(int k, bool frame_present);
+    std::vector<cudaGraphExec_t> graphs_;     // [ring slot][output-copy variant]
+    std::vector<long long> graph_launches_;
     void drain_completed(bool block_all);
     void flush_below(StreamHost& h, int64_t limit, std::vector<Out>& staged);
     std::shared_ptr<std::vector<uint8_t>> acquire_buffer();

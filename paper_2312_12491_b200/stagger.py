@@ -321,7 +321,8 @@ class Pipeline:
     deterministic mode per stream, pipeline.cpp:152-214)."""
 
     def __init__(self, cfg: EngineConfig, n_streams: int = 1, frame_bytes: int | None = None,
-                 max_skip: int = 0, ring_depth: int = 4, seeds=None, conds=None, negs=None, device: int = 0):
+                 max_skip: int = 0, ring_depth: int = 4, seeds=None, conds=None, negs=None, device: int = 0,
+                 graph: bool = False):
         self.cfg = cfg
         self.S = n_streams
         self.D = frame_bytes if frame_bytes is not None else cfg.d_latent
@@ -342,7 +343,7 @@ class Pipeline:
         elif cfg.negative_condition is not None:
             neg = np.tile(_f64(cfg.negative_condition, cfg.d_latent), (n_streams, 1))
         # The drop-in stream seed ordering: stream s uses seed base+s.
-        pc_cfg = L.sdx_pipeline_config(cfg.to_c(), n_streams, self.D, max_skip, ring_depth, 0)
+        pc_cfg = L.sdx_pipeline_config(cfg.to_c(), n_streams, self.D, max_skip, ring_depth, int(graph))
         self._seed_check = seeds
         if any(sd != cfg.seed + i for i, sd in enumerate(seeds)):
             raise InvalidArgument("Pipeline: stream seeds must be cfg.seed + stream index")
