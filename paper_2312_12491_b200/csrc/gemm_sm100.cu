@@ -259,24 +259,36 @@ __global__ void __launch_bounds__(320, 1)
         }
         __syncwarp();
     } else {
-        // epilogue warps 2..5 -> TMEM lane quadrants 2,3,0,1.  Per 32-column chunk:
-        // phase 1: tcgen05.ld 32 fp32 of the thread's row, scale + bias + per-image
-        // bias, staged in this warp's smem slab (row pitch 144 B);  phase 2: the warp
-        // re-reads the slab so 4 lanes cover one row's 32 columns, adds the residual,
-        // applies the activation and writes 16-byte coalesced stores.
+        // epilogue warps 2..9 -> TMEM lane quadrant warp % 4 (two warps per quadrant
+        // split the 32-column chunks).  Per chunk: phase 1: tcgen05.ld 32 fp32 of the
+        // thread's row, scale + bias + per-image bias (+ fused GEGLU), staged in this
+        // warp's XOR-swizzled smem slab;  phase 2: the warp re-reads the slab so 4 lanes
+        // cover one row's 32 columns, adds the residual, applies the activation,
+        // accumulates GroupNorm statistics and writes 16-byte coalesced stores.
+        // Every epilogue field is read into a scalar once (param space; no local copy).
         const int q = warp & 3;
-        const int half = (warp - 2) >> 2;  // two warps per lane quadrant split the 32-column chunks
-        GemmEpilogue e = g.epi;
-        if (splits > 1) {  // raw partial sums; splitk_reduce applies the real epilogue
-            e = GemmEpilogue{};
-            e.out_f32 = 1;
-            e.ld_out = g.N;
-        }
+        const int half = (warp - 2) >> 2;
+        const bool raw = splits > 1;  // split-K partials: plain fp32 sums, splitk_reduce finishes
+        const float e_scale = raw ? 1.f : g.epi.scale;
+        const float* e_bias = raw ? nullptr : g.epi.bias;
+        const float* e_bimg = raw ? nullptr : g.epi.bias_img;
+        const long long e_rpi = g.epi.rows_per_img;
+        const int* e_imgidx = g.epi.img_index;
+        const long long e_bimg_ld = g.epi.bias_img_ld ? g.epi.bias_img_ld : g.N;
+        const __nv_bfloat16* e_res = raw ? nullptr : g.epi.residual;
+        const long long e_ldres = g.epi.ld_res;
+        const int e_act = raw ? kActNone : g.epi.act;
+        const bool e_aar = !raw && g.epi.act_after_residual;
+        const int e_outk = raw ? 1 : g.epi.out_f32;
+        const long long e_ldo = raw ? g.N : g.epi.ld_out;
+        const int* e_omap = raw ? nullptr : g.epi.out_img_map;
+        const bool e_geglu = !raw && g.epi.geglu;
+        const int e_ngn = raw ? 0 : g.epi.n_gn;
         float* slab = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16) + (warp - 2) * (32 * 32);
         uint32_t lt = 0;
         for (int u = blockIdx.x; u < total; u += gridDim.x, ++lt) {
             const int t = u / splits;
-            if (splits > 1) e.out = g.ws + static_cast<long long>(u % splits) * g.M * g.N;
+            void* e_out = raw ? static_cast<void*>(g.ws + static_cast<long long>(u % splits) * g.M * g.N) : g.epi.out;
             const uint32_t acc = lt & 1;
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
@@ -284,9 +296,9 @@ __global__ void __launch_bounds__(320, 1)
             tc_fence_after();
             const int row = m0 + q * 32 + lane;
             const float* bimg = nullptr;
-            if (e.bias_img && row < m_eff) {
-                const long long im = static_cast<long long>(row) / e.rows_per_img;
-                bimg = e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : g.N);
+            if (e_bimg && row < m_eff) {
+                const long long im = static_cast<long long>(row) / e_rpi;
+                bimg = e_bimg + (e_imgidx ? e_imgidx[im] : im) * e_bimg_ld;
             }
             const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
@@ -299,24 +311,24 @@ __global__ void __launch_bounds__(320, 1)
                 const bool vec_ok = col0 + 32 <= g.N;
                 float v[32];
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * e.scale;
-                if (e.bias) {
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * e_scale;
+                if (e_bias) {
                     if (vec_ok) {
 #pragma unroll
                         for (int i = 0; i < 32; i += 4) {
-                            const float4 b = *reinterpret_cast<const float4*>(e.bias + col0 + i);
+                            const float4 b = *reinterpret_cast<const float4*>(e_bias + col0 + i);
                             v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
                         }
                     } else {
                         for (int i = 0; i < 32; ++i)
-                            if (col0 + i < g.N) v[i] += e.bias[col0 + i];
+                            if (col0 + i < g.N) v[i] += e_bias[col0 + i];
                     }
                 }
                 if (bimg) {
                     for (int i = 0; i < 32; ++i)
                         if (col0 + i < g.N) v[i] += bimg[col0 + i];
                 }
-                if (e.geglu) {  // interleaved [16 value | 16 gate] columns -> 16 outputs
+                if (e_geglu) {  // interleaved [16 value | 16 gate] columns -> 16 outputs
 #pragma unroll
                     for (int i = 0; i < 16; ++i) v[i] = v[i] * 0.5f * v[16 + i] * (1.f + erff(v[16 + i] * 0.70710678118654752f));
                 }
@@ -328,17 +340,27 @@ __global__ void __launch_bounds__(320, 1)
                     *reinterpret_cast<float4*>(srow + (((i >> 2) ^ (lane & 7)) << 2)) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                 __syncwarp();
                 // phase 2: lane -> (row, 8 columns); 4 lanes per row (2 for GEGLU's 16 outputs)
-                const int lpr_shift = e.geglu ? 1 : 2;
+                const int lpr_shift = e_geglu ? 1 : 2;
                 const int pc = (lane & ((1 << lpr_shift) - 1)) * 8;
-                const int nout = e.geglu ? g.N / 2 : g.N;
-                const int ocol0 = e.geglu ? col0 / 2 : col0;
+                const int nout = e_geglu ? g.N / 2 : g.N;
+                const int ocol0 = e_geglu ? col0 / 2 : col0;
+                const int gcol = ocol0 + pc;
+                // GroupNorm partial sums of this lane's 8 columns (<= 2 groups per sink)
+                float ga0 = 0.f, gq0 = 0.f, ga1 = 0.f, gq1 = 0.f, gb0 = 0.f, gr0 = 0.f, gb1 = 0.f, gr1 = 0.f;
+                int gsplit0 = 8, gsplit1 = 8;
+                if (e_ngn > 0) {
+                    const int ch0 = g.epi.gn[0].c_off + gcol;
+                    gsplit0 = (ch0 / g.epi.gn[0].cg + 1) * g.epi.gn[0].cg - ch0;
+                }
+                if (e_ngn > 1) {
+                    const int ch0 = g.epi.gn[1].c_off + gcol;
+                    gsplit1 = (ch0 / g.epi.gn[1].cg + 1) * g.epi.gn[1].cg - ch0;
+                }
 #pragma unroll 1
                 for (int rr = 0; rr < 32; rr += (32 >> lpr_shift)) {
                     const int lr = rr + (lane >> lpr_shift);
                     const int grow = m0 + q * 32 + lr;
-                    if (grow >= m_eff) continue;
-                    const int gcol = ocol0 + pc;
-                    if (gcol >= nout) continue;
+                    if (grow >= m_eff || gcol >= nout) continue;
                     const float* sr = slab + lr * 32;
                     float w8[8];
                     const float4 a0 = *reinterpret_cast<const float4*>(sr + ((((pc >> 2)) ^ (lr & 7)) << 2));
@@ -346,12 +368,12 @@ __global__ void __launch_bounds__(320, 1)
                     w8[0] = a0.x; w8[1] = a0.y; w8[2] = a0.z; w8[3] = a0.w;
                     w8[4] = a1.x; w8[5] = a1.y; w8[6] = a1.z; w8[7] = a1.w;
                     const bool full8 = gcol + 8 <= nout;
-                    if (!e.act_after_residual) {
+                    if (!e_aar && e_act != kActNone) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) w8[i] = act_fn(w8[i], e.act);
+                        for (int i = 0; i < 8; ++i) w8[i] = act_fn(w8[i], e_act);
                     }
-                    if (e.residual) {
-                        const __nv_bfloat16* rp = e.residual + static_cast<long long>(grow) * e.ld_res + gcol;
+                    if (e_res) {
+                        const __nv_bfloat16* rp = e_res + static_cast<long long>(grow) * e_ldres + gcol;
                         if (full8) {
                             const uint4 rv = *reinterpret_cast<const uint4*>(rp);
                             const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
@@ -361,29 +383,39 @@ __global__ void __launch_bounds__(320, 1)
                             for (int i = 0; i < 8 && gcol + i < nout; ++i) w8[i] += __bfloat162float(rp[i]);
                         }
                     }
-                    if (e.act_after_residual) {
+                    if (e_aar && e_act != kActNone) {
 #pragma unroll
-                        for (int i = 0; i < 8; ++i) w8[i] = act_fn(w8[i], e.act);
+                        for (int i = 0; i < 8; ++i) w8[i] = act_fn(w8[i], e_act);
+                    }
+                    if (e_ngn > 0) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const float rv = (gcol + i < nout) ? __bfloat162float(__float2bfloat16(w8[i])) : 0.f;
+                            if (i < gsplit0) { ga0 += rv; gq0 += rv * rv; } else { ga1 += rv; gq1 += rv * rv; }
+                            if (e_ngn > 1) {
+                                if (i < gsplit1) { gb0 += rv; gr0 += rv * rv; } else { gb1 += rv; gr1 += rv * rv; }
+                            }
+                        }
                     }
                     long long orow = grow;
-                    if (e.out_img_map) {
-                        const long long im = static_cast<long long>(grow) / e.rows_per_img;
-                        orow = static_cast<long long>(e.out_img_map[im]) * e.rows_per_img + (grow - im * e.rows_per_img);
+                    if (e_omap) {
+                        const long long im = static_cast<long long>(grow) / e_rpi;
+                        orow = static_cast<long long>(e_omap[im]) * e_rpi + (grow - im * e_rpi);
                     }
-                    if (e.out_f32 == 1) {
-                        float* op = reinterpret_cast<float*>(e.out) + orow * e.ld_out + gcol;
+                    if (e_outk == 1) {
+                        float* op = reinterpret_cast<float*>(e_out) + orow * e_ldo + gcol;
                         if (full8) {
                             *reinterpret_cast<float4*>(op) = make_float4(w8[0], w8[1], w8[2], w8[3]);
                             *reinterpret_cast<float4*>(op + 4) = make_float4(w8[4], w8[5], w8[6], w8[7]);
                         } else {
                             for (int i = 0; i < 8 && gcol + i < nout; ++i) op[i] = w8[i];
                         }
-                    } else if (e.out_f32 == 2) {
-                        uint8_t* op = reinterpret_cast<uint8_t*>(e.out) + orow * e.ld_out + gcol;
+                    } else if (e_outk == 2) {
+                        uint8_t* op = reinterpret_cast<uint8_t*>(e_out) + orow * e_ldo + gcol;
                         for (int i = 0; i < 8 && gcol + i < nout; ++i)
                             op[i] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(w8[i], 0.f), 1.f) * 255.f));
                     } else {
-                        __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + orow * e.ld_out + gcol;
+                        __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e_out) + orow * e_ldo + gcol;
                         if (full8) {
                             uint4 o;
                             o.x = pack_bf16(w8[0], w8[1]);
@@ -393,6 +425,35 @@ __global__ void __launch_bounds__(320, 1)
                             *reinterpret_cast<uint4*>(op) = o;
                         } else {
                             for (int i = 0; i < 8 && gcol + i < nout; ++i) op[i] = __float2bfloat16(w8[i]);
+                        }
+                    }
+                }
+                // lanes sharing columns (lane bits 2..4) combine; lanes 0..3 add one
+                // fixed-point atomic per (group, moment)
+                if (e_ngn > 0) {
+                    float gv[8] = {ga0, gq0, ga1, gq1, gb0, gr0, gb1, gr1};
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        gv[j] += __shfl_xor_sync(0xffffffffu, gv[j], 4);
+                        gv[j] += __shfl_xor_sync(0xffffffffu, gv[j], 8);
+                        gv[j] += __shfl_xor_sync(0xffffffffu, gv[j], 16);
+                    }
+                    const int wrow0 = m0 + q * 32;
+                    if (lane < 4 && gcol < nout && wrow0 < m_eff) {
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk) {
+                            if (kk >= e_ngn) break;
+                            const GnSink sk = kk == 0 ? g.epi.gn[0] : g.epi.gn[1];
+                            const int split = kk == 0 ? gsplit0 : gsplit1;
+                            const long long img = wrow0 / sk.hw;
+                            const int g0 = (sk.c_off + gcol) / sk.cg;
+                            unsigned long long* a0 = sk.acc + (img * sk.groups + g0) * 2;
+                            atomicAdd(a0, static_cast<unsigned long long>(__float2ll_rn(gv[4 * kk] * kGnFixedScale)));
+                            atomicAdd(a0 + 1, static_cast<unsigned long long>(__float2ll_rn(gv[4 * kk + 1] * kGnFixedScale)));
+                            if (split < 8 && g0 + 1 < sk.groups) {
+                                atomicAdd(a0 + 2, static_cast<unsigned long long>(__float2ll_rn(gv[4 * kk + 2] * kGnFixedScale)));
+                                atomicAdd(a0 + 3, static_cast<unsigned long long>(__float2ll_rn(gv[4 * kk + 3] * kGnFixedScale)));
+                            }
                         }
                     }
                 }
@@ -448,6 +509,27 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
             if (e.residual) x += __bfloat162float(e.residual[static_cast<long long>(row) * e.ld_res + col + i]);
             if (e.act_after_residual) x = act_fn(x, e.act);
             w[i] = x;
+        }
+        for (int kk = 0; kk < e.n_gn; ++kk) {  // GroupNorm statistics of the stored values
+            const GnSink& sk = e.gn[kk];
+            const int ch0 = sk.c_off + col;
+            const int g0 = ch0 / sk.cg;
+            const int b = (g0 + 1) * sk.cg - ch0;
+            float a[4] = {0.f, 0.f, 0.f, 0.f};
+            for (int i = 0; i < cnt; ++i) {
+                const float r = __bfloat162float(__float2bfloat16(w[i]));
+                const int hi = i >= b ? 2 : 0;
+                a[hi] += r;
+                a[hi + 1] += r * r;
+            }
+            const long long img = row / sk.hw;
+            unsigned long long* a0 = sk.acc + (img * sk.groups + g0) * 2;
+            atomicAdd(a0, static_cast<unsigned long long>(__float2ll_rn(a[0] * kGnFixedScale)));
+            atomicAdd(a0 + 1, static_cast<unsigned long long>(__float2ll_rn(a[1] * kGnFixedScale)));
+            if (b < cnt && g0 + 1 < sk.groups) {
+                atomicAdd(a0 + 2, static_cast<unsigned long long>(__float2ll_rn(a[2] * kGnFixedScale)));
+                atomicAdd(a0 + 3, static_cast<unsigned long long>(__float2ll_rn(a[3] * kGnFixedScale)));
+            }
         }
         long long orow = row;
         if (e.out_img_map) orow = static_cast<long long>(e.out_img_map[im]) * e.rows_per_img + (row - im * e.rows_per_img);

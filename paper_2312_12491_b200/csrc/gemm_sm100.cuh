@@ -21,6 +21,19 @@ namespace sdx {
 enum { kActNone = 0, kActSilu = 1, kActRelu = 2, kActGelu = 3 };
 enum { kAMatrix = 0, kAConcat = 1, kAConv = 2 };
 
+// GroupNorm statistics accumulated in the epilogue of the GEMM that produces
+// the normalised tensor: per (image, group) sum and sum of squares of the
+// stored (bf16-rounded) outputs as 2^-20 fixed-point int64 atomics, which are
+// exact and order-independent, so the statistics are deterministic.
+struct GnSink {
+    unsigned long long* acc = nullptr;  // [images][groups][2]
+    int c_off = 0;                      // channel offset of this tensor inside the GN input
+    int cg = 1;                         // channels per group
+    int groups = 32;
+    long long hw = 1;                   // rows per image
+};
+constexpr float kGnFixedScale = 1048576.f;  // 2^20
+
 struct GemmEpilogue {
     const float* bias = nullptr;          // [N]
     const float* bias_img = nullptr;      // [images][N] (time-embedding projection)
@@ -37,6 +50,8 @@ struct GemmEpilogue {
     int act_after_residual = 0;           // act(acc + bias + residual) instead of act(acc + bias) + residual
     int geglu = 0;                        // B rows interleaved [16 value | 16 gate]: out[:, j] = a_j * gelu(g_j), N/2 cols
     const int* out_img_map = nullptr;     // image -> destination image block of rows_per_img rows (scatter)
+    GnSink gn[2];                         // GroupNorm statistics of this output (up to two consumers)
+    int n_gn = 0;
     const int* rows_dev = nullptr;        // device row-unit count (skip tiles past *rows_dev * rows_per_unit)
     long long rows_per_unit = 0;
 };

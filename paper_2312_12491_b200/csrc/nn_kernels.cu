@@ -37,55 +37,87 @@ __device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); 
 
 // ---- GroupNorm ----------------------------------------------------------------
 
+// Thread layout of both GroupNorm kernels: blockDim = noct x PY, thread
+// (ox, py) owns channel octet ox (8 channels, <= 2 groups since Ct/32 >= 8) and
+// walks pixels py, py + PY, ...  with 4 independent 16-byte loads in flight.
+__device__ __forceinline__ const bf16* gn_src(const GnPlan& p, int img, int px, int c) {
+    return c < p.C1 ? p.x1 + (static_cast<long long>(img) * p.HW + px) * p.C1 + c
+                    : p.x2 + (static_cast<long long>(img) * p.HW + px) * p.C2 + (c - p.C1);
+}
+
 __global__ void gn_stats_kernel(GnPlan p) {
     const int img = blockIdx.y;
     if (p.rows_dev && img >= *p.rows_dev) return;
-    extern __shared__ float sm[];  // [per][2][Ct] per-thread partials, reduced in a fixed order
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
-    const int per = blockDim.x / noct;  // pixels processed concurrently
-    const int oct = threadIdx.x % noct;
-    const int pl = threadIdx.x / noct;
-    const int pp = (p.HW + p.chunks - 1) / p.chunks;
+    const int PY = blockDim.x / noct;
+    const int ox = threadIdx.x % noct, py = threadIdx.x / noct;
+    const int cg = Ct / p.groups;
+    const int c = ox * 8;
+    const int g0 = c / cg, split = (g0 + 1) * cg - c;
+    const int pp = PY * 8;  // pixels per block
     const int pix0 = blockIdx.x * pp;
-    const int pix1 = min(p.HW, pix0 + pp);
-    float s[8] = {0, 0, 0, 0, 0, 0, 0, 0}, q[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (pl < per) {
-        const int c = oct * 8;
-        const bool first = c < p.C1;
-        const bf16* base = first ? p.x1 + static_cast<long long>(img) * p.HW * p.C1 + c
-                                 : p.x2 + static_cast<long long>(img) * p.HW * p.C2 + (c - p.C1);
-        const int ld = first ? p.C1 : p.C2;
-        for (int px = pix0 + pl; px < pix1; px += per) {
-            float v[8];
-            load8(base + static_cast<long long>(px) * ld, v);
+    float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
+    if (py < PY) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                s[i] += v[i];
-                q[i] += v[i] * v[i];
+        for (int b = 0; b < 2; ++b) {
+            float v[4][8];
+            bool ok[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int px = pix0 + py + (b * 4 + k) * PY;
+                ok[k] = px < p.HW;
+                if (ok[k]) load8(gn_src(p, img, px, c), v[k]);
             }
-        }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            sm[(pl * 2) * Ct + c + i] = s[i];
-            sm[(pl * 2 + 1) * Ct + c + i] = q[i];
+            for (int k = 0; k < 4; ++k) {
+                if (!ok[k]) continue;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (i < split) {
+                        s0 += v[k][i];
+                        q0 += v[k][i] * v[k][i];
+                    } else {
+                        s1 += v[k][i];
+                        q1 += v[k][i] * v[k][i];
+                    }
+                }
+            }
         }
     }
+    // fixed-order reduction: per octet over pixel lanes, then per group over octets
+    extern __shared__ float sm[];  // [PY][noct][4]
+    float* mine = sm + (static_cast<long long>(py) * noct + ox) * 4;
+    if (py < PY) {
+        mine[0] = s0;
+        mine[1] = q0;
+        mine[2] = s1;
+        mine[3] = q1;
+    }
     __syncthreads();
-    const int cg = Ct / p.groups;
+    float red[4] = {0.f, 0.f, 0.f, 0.f};
+    if (threadIdx.x < noct)
+        for (int y = 0; y < PY; ++y)
+            for (int j = 0; j < 4; ++j) red[j] += sm[(static_cast<long long>(y) * noct + threadIdx.x) * 4 + j];
+    __syncthreads();
+    if (threadIdx.x < noct)
+        for (int j = 0; j < 4; ++j) sm[threadIdx.x * 4 + j] = red[j];
+    __syncthreads();
     for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
         float a = 0.f, b = 0.f;
-        for (int k = 0; k < per; ++k)
-            for (int c = g * cg; c < (g + 1) * cg; ++c) {
-                a += sm[(k * 2) * Ct + c];
-                b += sm[(k * 2 + 1) * Ct + c];
-            }
+        const int o0 = (g * cg) / 8, o1 = ((g + 1) * cg - 1) / 8;
+        for (int o = o0; o <= o1; ++o) {
+            const int oc = o * 8;
+            const int og0 = oc / cg;
+            const int part = og0 == g ? 0 : 2;  // this octet's first or second group
+            a += sm[o * 4 + part];
+            b += sm[o * 4 + part + 1];
+        }
         float* out = p.partial + ((static_cast<long long>(img) * p.chunks + blockIdx.x) * p.groups + g) * 2;
         out[0] = a;
         out[1] = b;
     }
-    // the last chunk of this image to finish reduces all chunks: one warp per group,
-    // fp64 partial sums in a fixed order (deterministic), mean / rstd for apply
+    // the last chunk of this image to finish reduces all chunks (fp64, fixed order)
     __shared__ unsigned int last;
     __threadfence();
     __syncthreads();
@@ -106,7 +138,7 @@ __global__ void gn_stats_kernel(GnPlan p) {
             b += __shfl_xor_sync(0xffffffffu, b, off);
         }
         if (lane == 0) {
-            const double n = static_cast<double>(Ct / p.groups) * p.HW;
+            const double n = static_cast<double>(cg) * p.HW;
             const double mean = a / n;
             double var = b / n - mean * mean;
             if (var < 0) var = 0;
@@ -117,43 +149,69 @@ __global__ void gn_stats_kernel(GnPlan p) {
     if (threadIdx.x == 0) p.counter[img] = 0;
 }
 
+__device__ __forceinline__ void gn_group_stats(const GnPlan& p, int img, int g, float* mean, float* rstd) {
+    if (p.acc) {
+        const int cg = (p.C1 + p.C2) / p.groups;
+        const double inv = 1.0 / 1048576.0;
+        const double n = static_cast<double>(cg) * p.HW;
+        const double m = static_cast<double>(static_cast<long long>(p.acc[(img * p.groups + g) * 2])) * inv / n;
+        double var = static_cast<double>(static_cast<long long>(p.acc[(img * p.groups + g) * 2 + 1])) * inv / n - m * m;
+        if (var < 0) var = 0;
+        *mean = static_cast<float>(m);
+        *rstd = static_cast<float>(1.0 / sqrt(var + p.eps));
+    } else {
+        *mean = p.stats[(img * p.groups + g) * 2];
+        *rstd = p.stats[(img * p.groups + g) * 2 + 1];
+    }
+}
+
 __global__ void gn_apply_kernel(GnPlan p) {
     const int img = blockIdx.y;
     if (p.rows_dev && img >= *p.rows_dev) return;
-    __shared__ float mean_s[64], rstd_s[64];
     const int Ct = p.C1 + p.C2;
-    const int cg = Ct / p.groups;
-    for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
-        mean_s[g] = p.stats[(img * p.groups + g) * 2];
-        rstd_s[g] = p.stats[(img * p.groups + g) * 2 + 1];
-    }
-    __syncthreads();
     const int noct = Ct / 8;
-    const int pp = (p.HW + gridDim.x - 1) / gridDim.x;
-    const int pix0 = blockIdx.x * pp;
-    const int pix1 = min(p.HW, pix0 + pp);
-    const long long total = static_cast<long long>(pix1 - pix0) * noct;
-    for (long long idx = threadIdx.x; idx < total; idx += blockDim.x) {
-        const int px = pix0 + static_cast<int>(idx / noct);
-        const int c = static_cast<int>(idx % noct) * 8;
-        const bool first = c < p.C1;
-        const bf16* src = first ? p.x1 + (static_cast<long long>(img) * p.HW + px) * p.C1 + c
-                                : p.x2 + (static_cast<long long>(img) * p.HW + px) * p.C2 + (c - p.C1);
-        float v[8];
-        load8(src, v);
-        const int g0 = c / cg;
-        const int gb = (g0 + 1) * cg;  // first channel of the next group
-        const float4 ga = *reinterpret_cast<const float4*>(p.gamma + c), gb4 = *reinterpret_cast<const float4*>(p.gamma + c + 4);
-        const float4 ba = *reinterpret_cast<const float4*>(p.beta + c), bb4 = *reinterpret_cast<const float4*>(p.beta + c + 4);
-        const float gam[8] = {ga.x, ga.y, ga.z, ga.w, gb4.x, gb4.y, gb4.z, gb4.w};
-        const float bet[8] = {ba.x, ba.y, ba.z, ba.w, bb4.x, bb4.y, bb4.z, bb4.w};
+    const int PY = blockDim.x / noct;
+    const int ox = threadIdx.x % noct, py = threadIdx.x / noct;
+    if (py >= PY) return;
+    const int cg = Ct / p.groups;
+    const int c = ox * 8;
+    const int g0 = c / cg, split = (g0 + 1) * cg - c;
+    float m0, r0, m1 = 0.f, r1 = 0.f;
+    gn_group_stats(p, img, g0, &m0, &r0);
+    if (split < 8) gn_group_stats(p, img, g0 + 1, &m1, &r1);
+    float sc[8], sh[8];  // y = x * sc + sh
+    {
+        const float4 ga = *reinterpret_cast<const float4*>(p.gamma + c), gb = *reinterpret_cast<const float4*>(p.gamma + c + 4);
+        const float4 ba = *reinterpret_cast<const float4*>(p.beta + c), bb = *reinterpret_cast<const float4*>(p.beta + c + 4);
+        const float gam[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const float bet[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int g = (c + i) < gb ? g0 : g0 + 1;  // an octet spans at most two groups (cg >= 8)
-            float y = (v[i] - mean_s[g]) * rstd_s[g] * gam[i] + bet[i];
-            v[i] = p.silu ? silu(y) : y;
+            const float m = i < split ? m0 : m1, r = i < split ? r0 : r1;
+            sc[i] = r * gam[i];
+            sh[i] = bet[i] - m * r * gam[i];
         }
-        store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v);
+    }
+    const int pp = PY * 4;
+    const int pix0 = blockIdx.x * pp;
+    float v[4][8];
+    bool ok[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int px = pix0 + py + k * PY;
+        ok[k] = px < p.HW;
+        if (ok[k]) load8(gn_src(p, img, px, c), v[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (!ok[k]) continue;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float y = v[k][i] * sc[i] + sh[i];
+            v[k][i] = p.silu ? silu(y) : y;
+        }
+        const int px = pix0 + py + k * PY;
+        store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v[k]);
     }
 }
 
@@ -373,16 +431,15 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
     p.out = out;
     p.imgs = imgs;
     p.rows_dev = rows_dev;
+    p.acc = nullptr;
     const int Ct = p.C1 + p.C2;
     if (Ct % 8 != 0 || Ct % p.groups != 0 || (p.C2 && p.C1 % 8 != 0))
         raise(SDX_INVALID_ARGUMENT, "groupnorm: channels must be multiples of 8 and 32");
-    // ~4 pixels per thread per stats block: enough blocks to keep HBM busy
+    // 8 pixels per thread per stats block (two batches of 4 loads in flight)
     const int noct = Ct / 8;
-    const int threads = noct >= 256 ? noct : noct * (256 / noct);
-    const int per = threads / noct;
-    int chunks = HW / (per * 4);
+    const int PY = noct >= 256 ? 1 : 256 / noct;
+    int chunks = (HW + PY * 8 - 1) / (PY * 8);
     if (chunks < 1) chunks = 1;
-    if (chunks > 1024) chunks = 1024;
     p.chunks = chunks;
     p.partial = dev_alloc<float>(static_cast<size_t>(imgs) * chunks * p.groups * 2);
     p.stats = dev_alloc<float>(static_cast<size_t>(imgs) * p.groups * 2);
@@ -401,15 +458,14 @@ void free_groupnorm(GnPlan& p) {
 void run_groupnorm(const GnPlan& p, cudaStream_t st) {
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
-    const int threads = noct >= 256 ? noct : noct * (256 / noct);
-    dim3 g1(p.chunks, p.imgs);
-    const int per = threads / noct;
-    gn_stats_kernel<<<g1, threads, static_cast<size_t>(per) * 2 * Ct * sizeof(float), st>>>(p);
-    SDX_LAUNCH_CHECK();
-    // apply: ~4 octets per thread
-    int ab = static_cast<int>((static_cast<long long>(p.HW) * noct + 1023) / 1024);
-    if (ab < 1) ab = 1;
-    gn_apply_kernel<<<dim3(ab, p.imgs), 256, 0, st>>>(p);
+    const int PY = noct >= 256 ? 1 : 256 / noct;
+    const int threads = noct * PY;
+    if (!p.acc) {  // statistics not fused into the producer: standalone pass
+        gn_stats_kernel<<<dim3(p.chunks, p.imgs), threads, static_cast<size_t>(threads) * 4 * sizeof(float), st>>>(p);
+        SDX_LAUNCH_CHECK();
+    }
+    const int ab = (p.HW + PY * 4 - 1) / (PY * 4);
+    gn_apply_kernel<<<dim3(ab, p.imgs), threads, 0, st>>>(p);
     SDX_LAUNCH_CHECK();
 }
 

@@ -23,6 +23,9 @@ struct GnPlan {
     float* partial;  // [imgs][chunks][groups][2]
     float* stats;    // [imgs][groups][2] mean, rstd (written by the last stats block per image)
     unsigned int* counter;  // [imgs] stats blocks finished
+    // fused statistics: sums accumulated by the producing GEMM epilogues (GnSink),
+    // 2^-20 fixed point; null -> the standalone stats kernel runs
+    const unsigned long long* acc;
     int chunks;
     int imgs;
     const int* rows_dev;

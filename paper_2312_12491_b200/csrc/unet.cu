@@ -2,6 +2,7 @@
 #include "unet.cuh"
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -47,8 +48,45 @@ float* UNet::actf(long long elems) {
 }
 
 void UNet::gemm_op(const std::string& kind, const GemmPlan& p) {
-    ops_.push_back(Op{kind, [p](cudaStream_t st) { run_gemm(p, st); }});
+    plans_.push_back(p);
+    GemmPlan* pp = &plans_.back();
+    ops_.push_back(Op{kind, [pp](cudaStream_t st) { run_gemm(*pp, st); }});
+    produced_[p.epi.out] = pp;
     flops_per_row_ += 2.0 * p.N * p.K * (static_cast<double>(p.M) / R_);
+}
+
+GnPlan UNet::groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, float eps, const float* g,
+                       const float* b, int silu, bf16* out) {
+    GnPlan gp = plan_groupnorm(x1, C1, x2, C2, HW, R_, eps, g, b, silu, out, rows_dev_);
+    auto p1 = produced_.find(x1);
+    auto p2 = x2 ? produced_.find(x2) : produced_.end();
+    const bool fusable = p1 != produced_.end() && p1->second->epi.n_gn < 2 && !p1->second->epi.geglu &&
+                         (!x2 || (p2 != produced_.end() && p2->second->epi.n_gn < 2 && !p2->second->epi.geglu));
+    const size_t need = static_cast<size_t>(R_) * gp.groups * 2;
+    // Epilogue-fused statistics measured slower than the standalone stats pass
+    // (atomic traffic in the producers' epilogues); opt in with SDX_GN_FUSE=1.
+    static const bool enabled = [] {
+        const char* v = std::getenv("SDX_GN_FUSE");
+        return v && v[0] == '1';
+    }();
+    if (enabled && fusable && gn_acc_used_ + need <= gn_acc_elems_) {
+        unsigned long long* acc = gn_acc_ + gn_acc_used_;
+        gn_acc_used_ += need;
+        const int Ct = C1 + (x2 ? C2 : 0);
+        GnSink s;
+        s.acc = acc;
+        s.cg = Ct / gp.groups;
+        s.groups = gp.groups;
+        s.hw = HW;
+        s.c_off = 0;
+        p1->second->epi.gn[p1->second->epi.n_gn++] = s;
+        if (x2) {
+            s.c_off = C1;
+            p2->second->epi.gn[p2->second->epi.n_gn++] = s;
+        }
+        gp.acc = acc;
+    }
+    return gp;
 }
 
 // ResnetBlock2D: GN+SiLU -> conv3x3 (+ time-embedding bias per row) -> GN+SiLU ->
@@ -63,7 +101,7 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
     {
         float* g = wf32(nm + ".norm1.g", {Cin}, 0.f, 1.f);
         float* b = wf32(nm + ".norm1.b", {Cin}, 0.f, 0.f);
-        GnPlan gp = plan_groupnorm(x, Cx, skip, Cs, HW, R_, 1e-5f, g, b, 1, t1, rows);
+        GnPlan gp = groupnorm(x, Cx, skip, Cs, HW, 1e-5f, g, b, 1, t1);
         gns_.push_back(gp);
         ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
     }
@@ -91,7 +129,7 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
     {
         float* g = wf32(nm + ".norm2.g", {Cout}, 0.f, 1.f);
         float* b = wf32(nm + ".norm2.b", {Cout}, 0.f, 0.f);
-        GnPlan gp = plan_groupnorm(h1, Cout, nullptr, 0, HW, R_, 1e-5f, g, b, 1, t2, rows);
+        GnPlan gp = groupnorm(h1, Cout, nullptr, 0, HW, 1e-5f, g, b, 1, t2);
         gns_.push_back(gp);
         ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
     }
@@ -152,7 +190,7 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
     {
         float* g = wf32(nm + ".norm.g", {C}, 0.f, 1.f);
         float* b = wf32(nm + ".norm.b", {C}, 0.f, 0.f);
-        GnPlan gp = plan_groupnorm(x, C, nullptr, 0, HW, R_, 1e-6f, g, b, 0, t, rows);
+        GnPlan gp = groupnorm(x, C, nullptr, 0, HW, 1e-6f, g, b, 0, t);
         gns_.push_back(gp);
         ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
     }
@@ -271,6 +309,9 @@ UNet::UNet(const UNetConfig& cfg, cudaStream_t st) : cfg_(cfg) {
     const int init_rows[2] = {R_, R_};
     SDX_CUDA(cudaMemcpy(rows_buf_, init_rows, sizeof(init_rows), cudaMemcpyHostToDevice));
     rows_dev_ = rows_buf_;  // every planned op reads the live row count from rows_buf_[0]
+    gn_acc_elems_ = static_cast<size_t>(96) * R_ * 32 * 2;
+    gn_acc_ = dev_alloc<unsigned long long>(gn_acc_elems_);
+    allocs_.push_back(gn_acc_);
     ctx_ = act(static_cast<long long>(cfg.n_prompts) * cfg.ctx_len * cfg.ctx_dim);
     fill_normal_bf16(ctx_, static_cast<long long>(cfg.n_prompts) * cfg.ctx_len * cfg.ctx_dim, 1.f, cfg.seed ^ 0xC0FFEE, nullptr);
     params_.push_back(Param{"context", ctx_, {cfg.n_prompts, cfg.ctx_len, cfg.ctx_dim}, false});
@@ -354,7 +395,7 @@ UNet::UNet(const UNetConfig& cfg, cudaStream_t st) : cfg_(cfg) {
     {
         float* g = wf32("norm_out.g", {cur}, 0.f, 1.f);
         float* b = wf32("norm_out.b", {cur}, 0.f, 0.f);
-        GnPlan gp = plan_groupnorm(h, cur, nullptr, 0, H * W, R_, 1e-5f, g, b, 1, t, rows_dev_);
+        GnPlan gp = groupnorm(h, cur, nullptr, 0, H * W, 1e-5f, g, b, 1, t);
         gns_.push_back(gp);
         ops_.push_back(Op{"groupnorm", [gp](cudaStream_t s) { run_groupnorm(gp, s); }});
     }
@@ -412,12 +453,14 @@ void UNet::refresh_context(cudaStream_t st) {
 void UNet::forward(const int* rows_dev, cudaStream_t st) {
     if (rows_dev) SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_dev, sizeof(int), cudaMemcpyDeviceToDevice, st));
     else SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_buf_ + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    SDX_CUDA(cudaMemsetAsync(gn_acc_, 0, gn_acc_used_ * sizeof(unsigned long long), st));
     for (auto& op : ops_) op.fn(st);
 }
 
 void UNet::forward_profiled(const int* rows_dev, cudaStream_t st, std::vector<std::pair<std::string, float>>* out) {
     if (rows_dev) SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_dev, sizeof(int), cudaMemcpyDeviceToDevice, st));
     else SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_buf_ + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    SDX_CUDA(cudaMemsetAsync(gn_acc_, 0, gn_acc_used_ * sizeof(unsigned long long), st));
     std::vector<cudaEvent_t> ev(ops_.size() + 1);
     for (auto& e : ev) SDX_CUDA(cudaEventCreate(&e));
     SDX_CUDA(cudaEventRecord(ev[0], st));

@@ -18,7 +18,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <deque>
 #include <functional>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -81,6 +83,13 @@ class UNet {
     bf16* downsample(const bf16* x, int C, int H, int W, const std::string& nm);
     bf16* upsample(const bf16* x, int C, int H, int W, const std::string& nm);
     void gemm_op(const std::string& kind, const GemmPlan& p);
+    // GroupNorm over [x1 | x2]: statistics fused into the producing GEMMs' epilogues
+    GnPlan groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, float eps, const float* g,
+                     const float* b, int silu, bf16* out);
+    std::deque<GemmPlan> plans_;                 // stable storage: ops and GN sinks point into it
+    std::map<const void*, GemmPlan*> produced_;  // output tensor -> producing GEMM
+    unsigned long long* gn_acc_ = nullptr;       // fixed-point GN statistics arena, zeroed per forward
+    size_t gn_acc_elems_ = 0, gn_acc_used_ = 0;
 
     UNetConfig cfg_;
     std::vector<Param> params_;
