@@ -201,10 +201,22 @@ __global__ void __launch_bounds__(320, 1)
                 tmem_ld32_nowait(s_addr + 96, sr + 96);
                 tmem_wait_ld();
                 const int kv_valid = a.kv_len - j * BKV;
-                float mx = -INFINITY;
+                if (kv_valid < BKV) {  // partial last block: masked keys read as -inf
 #pragma unroll
-                for (int i = 0; i < BKV; ++i)
-                    if (i < kv_valid) mx = fmaxf(mx, __uint_as_float(sr[i]));
+                    for (int i = 0; i < BKV; ++i)
+                        if (i >= kv_valid) sr[i] = 0xff800000u;
+                }
+                // row max: 8 independent chains, then a tree
+                float mx8[8];
+#pragma unroll
+                for (int k = 0; k < 8; ++k) mx8[k] = __uint_as_float(sr[k]);
+#pragma unroll
+                for (int i = 8; i < BKV; i += 8) {
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], __uint_as_float(sr[i + k]));
+                }
+                const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                       fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
                 const float m_row = mx * sl2;
                 if (j > 0) wait_bar(&pv_done[t], (j - 1) & 1);  // PV(j-1) finished reading P_t and writing O_t
                 if (m_row > m_used + 8.f) {
@@ -225,15 +237,17 @@ __global__ void __launch_bounds__(320, 1)
                     l *= corr;
                     m_used = m_new;
                 }
-                float sum = 0.f;
+                // p = exp2(s * scale_log2 - m_used) (exp2(-inf) = 0 for masked keys), 8 partial sums
+                float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                const float nm = -m_used;
 #pragma unroll
                 for (int c = 0; c < BKV; c += 16) {
                     uint32_t pk[8];
 #pragma unroll
                     for (int i = 0; i < 16; i += 2) {
-                        const float p0 = (c + i < kv_valid) ? ex2(fmaf(__uint_as_float(sr[c + i]), sl2, -m_used)) : 0.f;
-                        const float p1 = (c + i + 1 < kv_valid) ? ex2(fmaf(__uint_as_float(sr[c + i + 1]), sl2, -m_used)) : 0.f;
-                        sum += p0 + p1;
+                        const float p0 = ex2(fmaf(__uint_as_float(sr[c + i]), sl2, nm));
+                        const float p1 = ex2(fmaf(__uint_as_float(sr[c + i + 1]), sl2, nm));
+                        sum8[i >> 1] += p0 + p1;
                         pk[i / 2] = pack_bf16(p0, p1);
                     }
                     uint8_t* atom = prow + (c >> 6) * TILE_BYTES + r * 128;
@@ -241,7 +255,7 @@ __global__ void __launch_bounds__(320, 1)
                     *reinterpret_cast<uint4*>(atom + (((ch0) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     *reinterpret_cast<uint4*>(atom + (((ch0 + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
                 }
-                l += sum;
+                l += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
                 fence_async_smem();
                 tc_fence_before();
                 mbar_arrive(&p_full[t]);

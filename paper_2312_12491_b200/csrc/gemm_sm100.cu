@@ -9,6 +9,7 @@
 //               bias / activation / residual in fp32, bf16 or fp32 stores
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -414,6 +415,19 @@ __global__ void __launch_bounds__(320, 1)
                         uint8_t* op = reinterpret_cast<uint8_t*>(e_out) + orow * e_ldo + gcol;
                         for (int i = 0; i < 8 && gcol + i < nout; ++i)
                             op[i] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(w8[i], 0.f), 1.f) * 255.f));
+                    } else if (e_outk == 3) {  // fp16 (attention operands)
+                        __half* op = reinterpret_cast<__half*>(e_out) + orow * e_ldo + gcol;
+                        if (full8) {
+                            uint4 o;
+                            __half2* h2 = reinterpret_cast<__half2*>(&o);
+                            h2[0] = __floats2half2_rn(w8[0], w8[1]);
+                            h2[1] = __floats2half2_rn(w8[2], w8[3]);
+                            h2[2] = __floats2half2_rn(w8[4], w8[5]);
+                            h2[3] = __floats2half2_rn(w8[6], w8[7]);
+                            *reinterpret_cast<uint4*>(op) = o;
+                        } else {
+                            for (int i = 0; i < 8 && gcol + i < nout; ++i) op[i] = __float2half_rn(w8[i]);
+                        }
                     } else {
                         __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e_out) + orow * e_ldo + gcol;
                         if (full8) {

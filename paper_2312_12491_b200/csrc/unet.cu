@@ -454,7 +454,14 @@ void UNet::forward(const int* rows_dev, cudaStream_t st) {
     if (rows_dev) SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_dev, sizeof(int), cudaMemcpyDeviceToDevice, st));
     else SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_buf_ + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
     SDX_CUDA(cudaMemsetAsync(gn_acc_, 0, gn_acc_used_ * sizeof(unsigned long long), st));
-    for (auto& op : ops_) op.fn(st);
+    // SDX_ABLATE="kind,kind": timing ablation for performance analysis only (skips op
+    // kinds, results are then wrong); never set in tests or the bench.
+    static const std::string ablate = [] {
+        const char* v = std::getenv("SDX_ABLATE");
+        return v ? std::string(",") + v + "," : std::string();
+    }();
+    for (auto& op : ops_)
+        if (ablate.empty() || ablate.find("," + op.kind + ",") == std::string::npos) op.fn(st);
 }
 
 void UNet::forward_profiled(const int* rows_dev, cudaStream_t st, std::vector<std::pair<std::string, float>>* out) {
