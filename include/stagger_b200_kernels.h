@@ -54,6 +54,8 @@ int sdx_unet_param_count(sdx_unet* u, int* n);
 int sdx_unet_param(sdx_unet* u, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32);
 int sdx_unet_flops_per_row(sdx_unet* u, double* flops);
 int sdx_unet_profile(sdx_unet* u, int rows, int cap, const char** kinds, float* ms, int* count);
+int sdx_unet_profile_detail(sdx_unet* u, int rows, int cap, const char** labels, double* flops, float* ms,
+                            int* count);
 int sdx_memcpy_d2d(void* dst, const void* src, int64_t bytes);
 /* cudaProfilerStart / Stop around a region (for ncu --profile-from-start off). */
 int sdx_profiler_start(void);

@@ -175,6 +175,25 @@ int sdx_unet_profile(sdx_unet* u, int rows, int cap, const char** kinds, float* 
     });
 }
 
+// Same, with each op's label (kind + GEMM/attention shape) and algorithmic FLOPs at rmax rows.
+int sdx_unet_profile_detail(sdx_unet* u, int rows, int cap, const char** labels, double* flops, float* ms,
+                            int* count) {
+    return kguard([&] {
+        static thread_local int* d_rows = nullptr;
+        static thread_local std::vector<std::pair<std::string, float>> res;
+        if (!d_rows) SDX_CUDA(cudaMalloc(&d_rows, sizeof(int)));
+        SDX_CUDA(cudaMemcpy(d_rows, &rows, sizeof(int), cudaMemcpyHostToDevice));
+        u->net->forward_profiled(d_rows, nullptr, &res);
+        const int n = static_cast<int>(res.size());
+        for (int i = 0; i < n && i < cap; ++i) {
+            labels[i] = u->net->op_label(static_cast<size_t>(i)).c_str();
+            flops[i] = u->net->op_flops(static_cast<size_t>(i));
+            ms[i] = res[static_cast<size_t>(i)].second;
+        }
+        *count = n;
+    });
+}
+
 int sdx_memcpy_d2d(void* dst, const void* src, int64_t bytes) {
     return kguard([&] { SDX_CUDA(cudaMemcpy(dst, src, static_cast<size_t>(bytes), cudaMemcpyDeviceToDevice)); });
 }

@@ -2,6 +2,7 @@
 #include "unet.cuh"
 
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -50,7 +51,9 @@ float* UNet::actf(long long elems) {
 void UNet::gemm_op(const std::string& kind, const GemmPlan& p) {
     plans_.push_back(p);
     GemmPlan* pp = &plans_.back();
-    ops_.push_back(Op{kind, [pp](cudaStream_t st) { run_gemm(*pp, st); }});
+    char lab[160];
+    std::snprintf(lab, sizeof lab, "%s M=%d N=%d K=%d bn=%d splits=%d", kind.c_str(), p.M, p.N, p.K, p.bn, p.splits);
+    ops_.push_back(Op{kind, [pp](cudaStream_t st) { run_gemm(*pp, st); }, lab, 2.0 * p.M * p.N * p.K});
     produced_[p.epi.out] = pp;
     flops_per_row_ += 2.0 * p.N * p.K * (static_cast<double>(p.M) / R_);
 }
@@ -205,7 +208,9 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
     {
         AttnPlan ap = plan_attention(qkv, M, 3 * C, 0, qkv, M, 3 * C, C, 2 * C, a1, C, 0, R_, heads, HW, HW, HW, HW,
                                      nullptr, rows, 0.125f);
-        ops_.push_back(Op{"attention", [ap](cudaStream_t st) { run_attention(ap, st); }});
+        ops_.push_back(Op{"attention", [ap](cudaStream_t st) { run_attention(ap, st); },
+                          "self-attention T=" + std::to_string(HW) + " heads=" + std::to_string(heads),
+                          4.0 * HW * HW * C * R_});
         flops_per_row_ += 4.0 * HW * HW * C;
     }
     bf16* h2 = act(M * C);
@@ -228,7 +233,9 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
     {
         AttnPlan ap = plan_attention(q, M, C, 0, kv, static_cast<long long>(P) * cfg_.ctx_len, 2 * C, 0, C, a2, C, 0,
                                      R_, heads, HW, HW, cfg_.ctx_len, cfg_.ctx_len, row_prompt_, rows, 0.125f);
-        ops_.push_back(Op{"attention", [ap](cudaStream_t st) { run_attention(ap, st); }});
+        ops_.push_back(Op{"attention", [ap](cudaStream_t st) { run_attention(ap, st); },
+                          "cross-attention T=" + std::to_string(HW) + " heads=" + std::to_string(heads),
+                          4.0 * HW * cfg_.ctx_len * C * R_});
         flops_per_row_ += 4.0 * HW * cfg_.ctx_len * C;
     }
     bf16* h3 = act(M * C);

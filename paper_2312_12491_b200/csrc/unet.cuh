@@ -68,11 +68,16 @@ class UNet {
     const UNetConfig& config() const { return cfg_; }
     // Device time of each op class accumulated by forward_profiled (ms).
     void forward_profiled(const int* rows_dev, cudaStream_t st, std::vector<std::pair<std::string, float>>* out);
+    // Per-op label (kind + shape) and FLOPs at rmax rows, in launch order.
+    const std::string& op_label(size_t i) const { return ops_[i].label.empty() ? ops_[i].kind : ops_[i].label; }
+    double op_flops(size_t i) const { return ops_[i].flops; }
 
   private:
     struct Op {
         std::string kind;
         std::function<void(cudaStream_t)> fn;
+        std::string label;   // kind + shape (profiling)
+        double flops = 0;    // algorithmic FLOPs at rmax rows (tensor ops)
     };
     bf16* wbf(const std::string& name, std::vector<long long> shape, float std);
     float* wf32(const std::string& name, std::vector<long long> shape, float std, float constant);
