@@ -40,6 +40,23 @@ int sdx_kernel_attention(const void* q, int64_t q_rows_total, int64_t ld_q, int 
                          float scale, void* stream);
 const char* sdx_kernel_last_error(void);
 
+/* Prebuilt GEMM / conv launches for kernel benchmarks: plan once (tensor maps,
+ * split-K workspace), replay `iters` times back to back on `stream`.
+ * force_bn / force_splits override the cost-model tiling (0 = model). */
+typedef struct sdx_gemm_plan sdx_gemm_plan;
+int sdx_kernel_gemm_plan(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int M, int N, int K,
+                         const float* bias, const void* residual, int act, int out_f32, int force_bn,
+                         int force_splits, sdx_gemm_plan** out);
+int sdx_kernel_conv3x3_plan(const void* x, int imgs, int H, int W, int Cin, const void* w, int Cout, int stride,
+                            const float* bias, const void* residual, int act, void* out, int out_f32, int force_bn,
+                            int force_splits, sdx_gemm_plan** out_plan);
+int sdx_kernel_plan_run(sdx_gemm_plan* p, int iters, void* stream);
+int sdx_kernel_plan_info(sdx_gemm_plan* p, int* bn, int* splits, double* model_clk);
+int sdx_kernel_plan_destroy(sdx_gemm_plan* p);
+/* Device u64 buffer [grid][8] for per-CTA %globaltimer phase stamps of the next
+ * GEMM launches (NULL disables); see set_gemm_debug_buffer in gemm_sm100.cuh. */
+int sdx_kernel_gemm_debug(void* dbg);
+
 /* The batched UNet denoiser (random-init SD-2.1/SD-turbo topology, bf16
  * weights, fp32 accumulation) used by the pipeline's predict_eps_batch slot.
  * taus: timestep of each schedule step; forward() takes rows latents x

@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(320, 1)
     const int qp = blockIdx.x;  // pair of q tiles
     const int head = blockIdx.y;
     const int img = blockIdx.z;
-    if (a.rows_dev && img >= *a.rows_dev) return;
+    if (threadIdx.x == 0) pdl_launch();
     const bool has1 = qp * 2 * BQ + BQ < a.q_len;  // second tile holds live queries
 
     extern __shared__ uint8_t smem_raw[];
@@ -123,8 +123,11 @@ __global__ void __launch_bounds__(320, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // TMEM columns: tile t: S at t*192, O at t*192 + 128
+    pdl_wait();  // setup above overlaps the previous kernel (PDL)
+    const bool live = !(a.rows_dev && img >= *a.rows_dev);
 
-    if (warp == 0) {
+    if (!live) {
+    } else if (warp == 0) {
         if (lane == 0) {
             mbar_expect_tx(q_full, (has1 ? 2 : 1) * TILE_BYTES);
             tma_load_2d(sQ, &tq, q_full, a.q_col0 + head * HD, q_row0);
@@ -350,8 +353,7 @@ void run_attention(const AttnPlan& p, cudaStream_t st) {
         attr = true;
     }
     dim3 grid((p.a.q_len + 2 * BQ - 1) / (2 * BQ), p.heads, p.images);
-    attn_kernel<<<grid, 320, smem, st>>>(p.tq, p.tkv, p.a);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(attn_kernel, grid, dim3(320), smem, st, p.tq, p.tkv, p.a);
 }
 
 }  // namespace sdx

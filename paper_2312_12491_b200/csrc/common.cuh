@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <stdexcept>
 #include <string>
 
@@ -28,6 +30,41 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 
 #define SDX_CUDA(x) ::sdx::cuda_check((x), #x, __FILE__, __LINE__)
 #define SDX_LAUNCH_CHECK() ::sdx::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__)
+
+// ---- programmatic dependent launch (PDL) ---------------------------------------
+// Kernels of the denoiser forward are launched with programmatic stream
+// serialisation: a kernel may start (prologue, TMEM alloc, descriptor and
+// weight prefetch) while its predecessor drains.  Every such kernel calls
+// pdl_launch() early and pdl_wait() before touching memory written by earlier
+// kernels (and before finishing), so ordering stays transitive.  SDX_PDL=0
+// disables it (plain stream order).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("SDX_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cuda_check(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), "cudaLaunchKernelEx", __FILE__, __LINE__);
+}
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+#endif
 
 constexpr int kMaxSteps = 64;     // n_steps upper bound for device slot tables
 constexpr int kSmCount = 148;     // B200

@@ -26,13 +26,22 @@ using namespace sm100;
 
 namespace {
 
+unsigned long long* g_dbg = nullptr;  // phase timestamps of the next launches (kernel benchmarks)
+
 struct GemmArgs {
     int M, N, K, K1, amode;
     int Ho, Wo, Cin, stride, Wt, Ht, Nt;
     int splits;   // split-K factor (> 1: raw fp32 partials to ws, epilogue in splitk_reduce)
     float* ws;    // [splits][M][N]
+    unsigned long long* dbg;  // optional per-CTA phase timestamps [grid][8] (kernel benchmarks)
     GemmEpilogue epi;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t) : : "memory");
+    return t;
+}
 
 __device__ __forceinline__ void wait_bounded(uint64_t* bar, uint32_t phase) {
     // mbarrier wait with a watchdog: a protocol bug traps instead of hanging the GPU
@@ -65,105 +74,25 @@ __device__ __forceinline__ float act_fn(float v, int act) {
     }
 }
 
-// bias / per-image bias / residual / activation on 16 accumulator columns of
-// one row, then a bf16, fp32 or u8 store.
-__device__ __forceinline__ void epilogue16(const GemmEpilogue& e, int N, long long row, long long orow, int col0,
-                                           const float* bimg, float* v) {
-    const bool full16 = col0 + 16 <= N;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-        const int col = col0 + i;
-        float x = v[i] * e.scale;
-        if (full16 || col < N) {
-            if (e.bias) x += e.bias[col];
-            if (bimg) x += bimg[col];
-        }
-        v[i] = x;
-    }
-    if (!e.act_after_residual) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = act_fn(v[i], e.act);
-    }
-    if (e.residual) {
-        const __nv_bfloat16* rp = e.residual + row * e.ld_res + col0;
-        if (full16) {
-            const uint4 r0 = *reinterpret_cast<const uint4*>(rp);
-            const uint4 r1 = *reinterpret_cast<const uint4*>(rp + 8);
-            const __nv_bfloat16* rb0 = reinterpret_cast<const __nv_bfloat16*>(&r0);
-            const __nv_bfloat16* rb1 = reinterpret_cast<const __nv_bfloat16*>(&r1);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                v[i] += __bfloat162float(rb0[i]);
-                v[8 + i] += __bfloat162float(rb1[i]);
-            }
-        } else {
-            for (int i = 0; i < 16 && col0 + i < N; ++i) v[i] += __bfloat162float(rp[i]);
-        }
-    }
-    if (e.act_after_residual) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = act_fn(v[i], e.act);
-    }
-    if (e.out_f32 == 1) {
-        float* op = reinterpret_cast<float*>(e.out) + orow * e.ld_out + col0;
-        if (full16) {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-        } else {
-            for (int i = 0; i < 16 && col0 + i < N; ++i) op[i] = v[i];
-        }
-    } else if (e.out_f32 == 2) {
-        uint8_t* op = reinterpret_cast<uint8_t*>(e.out) + orow * e.ld_out + col0;
-        for (int i = 0; i < 16 && col0 + i < N; ++i)
-            op[i] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(v[i], 0.f), 1.f) * 255.f));
-    } else {
-        __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + orow * e.ld_out + col0;
-        if (full16) {
-            uint4 o0, o1;
-            o0.x = pack_bf16(v[0], v[1]);
-            o0.y = pack_bf16(v[2], v[3]);
-            o0.z = pack_bf16(v[4], v[5]);
-            o0.w = pack_bf16(v[6], v[7]);
-            o1.x = pack_bf16(v[8], v[9]);
-            o1.y = pack_bf16(v[10], v[11]);
-            o1.z = pack_bf16(v[12], v[13]);
-            o1.w = pack_bf16(v[14], v[15]);
-            *reinterpret_cast<uint4*>(op) = o0;
-            *reinterpret_cast<uint4*>(op + 8) = o1;
-        } else {
-            for (int i = 0; i < 16 && col0 + i < N; ++i) op[i] = __float2bfloat16(v[i]);
-        }
-    }
-}
-
 // Persistent: grid = min(tiles, SMs); tiles in (m, n) order with n fastest so
 // consecutive tiles share the A block in L2.  Two TMEM accumulators let the
 // epilogue of tile i overlap the MMAs of tile i+1.
-template <int BN, int STAGES, int AMODE>
+template <int BN, int STAGES, int AMODE, bool FAST>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
-                   const __grid_constant__ CUtensorMap tb, const GemmArgs g) {
+                   const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap to, const GemmArgs g) {
     constexpr int BM = 128, BK = 64;
     constexpr uint32_t A_BYTES = BM * BK * 2;
     constexpr uint32_t B_BYTES = BN * BK * 2;
     constexpr uint32_t TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
 
-    int m_eff = g.M;
-    if (g.epi.rows_dev) {
-        const long long lim = static_cast<long long>(*g.epi.rows_dev) * g.epi.rows_per_unit;
-        if (lim < m_eff) m_eff = static_cast<int>(lim);
-    }
-    const int n_tiles = (g.N + BN - 1) / BN;
-    const int m_tiles = (m_eff + BM - 1) / BM;  // device-decided batch: only live rows' tiles
-    const int splits = g.splits;
-    const int total = m_tiles * n_tiles * splits;  // work units: (tile, K split)
-    if (static_cast<int>(blockIdx.x) >= total) return;
-
+    if (threadIdx.x == 0) pdl_launch();
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint8_t* slabs = sB + STAGES * B_BYTES;  // 8 epilogue warps x 4 KB (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(slabs + 8 * 4096);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;   // [2]
     uint64_t* tempty = tfull + 2;       // [2]
@@ -172,11 +101,14 @@ __global__ void __launch_bounds__(320, 1)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int nk = g.K / BK;
+    unsigned long long* dbg = g.dbg ? g.dbg + blockIdx.x * 16 : nullptr;
+    if (dbg && threadIdx.x == 0) dbg[0] = gtimer();
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&ta);
         if (AMODE == kAConcat) tma_prefetch(&ta2);
         tma_prefetch(&tb);
+        if (FAST) tma_prefetch(&to);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -192,6 +124,19 @@ __global__ void __launch_bounds__(320, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
+    // everything above overlaps the previous kernel's tail (PDL); from here on
+    // memory written by earlier kernels (incl. the live row count) is read
+    pdl_wait();
+    int m_eff = g.M;
+    if (g.epi.rows_dev) {
+        const long long lim = static_cast<long long>(*g.epi.rows_dev) * g.epi.rows_per_unit;
+        if (lim < m_eff) m_eff = static_cast<int>(lim);
+    }
+    const int n_tiles = (g.N + BN - 1) / BN;
+    const int m_tiles = (m_eff + BM - 1) / BM;  // device-decided batch: only live rows' tiles
+    const int splits = g.splits;
+    const int total = m_tiles * n_tiles * splits;  // work units: (tile, K split); CTAs past it idle
 
     if (warp == 0) {
         if (lane == 0) {
@@ -247,6 +192,7 @@ __global__ void __launch_bounds__(320, 1)
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     wait_bounded(&full[s], ph);
+                    if (dbg && it == 0) dbg[2] = gtimer();
                     tc_fence_after();
                     const uint64_t da = desc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
                     const uint64_t db = desc_kmajor_sw128(smem_u32(sB + s * B_BYTES));
@@ -256,8 +202,191 @@ __global__ void __launch_bounds__(320, 1)
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
+                if (dbg && lt == 0) dbg[3] = gtimer();
             }
         }
+        __syncwarp();
+    } else if constexpr (FAST) {
+        // Streamlined epilogue (bf16 output, or the fp32 split-K partials): each
+        // thread owns one TMEM lane = one output row; per 32-column chunk
+        // tcgen05.ld -> scale / bias / per-image bias / ReLU / residual in
+        // registers -> 64-byte rows into a 64B-swizzled smem box -> one TMA
+        // store per warp (OOB rows / columns clipped by the tensor map).  The
+        // residual row segment is fetched before the TMEM load.
+        const int q = warp & 3;
+        const int half = (warp - 2) >> 2;
+        const bool raw = splits > 1;
+        const float e_scale = raw ? 1.f : g.epi.scale;
+        const float* e_bias = raw ? nullptr : g.epi.bias;
+        const float* e_bimg = raw ? nullptr : g.epi.bias_img;
+        const long long e_rpi = g.epi.rows_per_img;
+        const int* e_imgidx = g.epi.img_index;
+        const long long e_bimg_ld = g.epi.bias_img_ld ? g.epi.bias_img_ld : g.N;
+        const __nv_bfloat16* e_res = raw ? nullptr : g.epi.residual;
+        const long long e_ldres = g.epi.ld_res;
+        const bool e_relu = !raw && g.epi.act == kActRelu;
+        const bool e_aar = !raw && g.epi.act_after_residual;
+        const bool e_geglu = !raw && g.epi.geglu;
+        uint8_t* slab = slabs + (warp - 2) * 4096;
+        const uint32_t slab_s = smem_u32(slab);
+        uint32_t nstore = 0;  // bf16 boxes issued by this warp (double-buffered 2 KB halves)
+        uint32_t lt = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x, ++lt) {
+            const int t = u / splits;
+            const int sp = u - t * splits;
+            const uint32_t acc = lt & 1;
+            const int m0 = (t / n_tiles) * BM;
+            const int n0 = (t % n_tiles) * BN;
+            const int row0 = m0 + q * 32;
+            const int row = row0 + lane;
+            wait_bounded(&tfull[acc], (lt >> 1) & 1);
+            if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[4] = gtimer();
+            tc_fence_after();
+            const float* bimg = nullptr;
+            if (e_bimg && row < m_eff) {
+                const long long im = static_cast<long long>(row) / e_rpi;
+                bimg = e_bimg + (e_imgidx ? e_imgidx[im] : im) * e_bimg_ld;
+            }
+            const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll 1
+            for (int c = half * 32; c < BN; c += 64) {
+                const int col0 = n0 + c;
+                if (col0 >= g.N) break;  // warp-uniform; N % 32 == 0 on this path
+                uint4 rq[4];
+                if (e_res) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(e_res + static_cast<long long>(row < m_eff ? row : 0) * e_ldres + col0);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) rq[i] = rp[i];
+                }
+                uint32_t r[32];
+                tmem_ld32_nowait(tbase + c, r);
+                tmem_wait_ld();
+                const bool dstamp = dbg && lt == 0 && warp == 2 && lane == 0;
+                if (dstamp) dbg[7 + 3 * (c / 64)] = gtimer();
+                float v[32];
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * e_scale;
+                if (e_bias) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 b = *reinterpret_cast<const float4*>(e_bias + col0 + i);
+                        v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+                    }
+                }
+                if (bimg) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 b = *reinterpret_cast<const float4*>(bimg + col0 + i);
+                        v[i] += b.x; v[i + 1] += b.y; v[i + 2] += b.z; v[i + 3] += b.w;
+                    }
+                }
+                if (e_relu && !e_aar) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+                }
+                if (e_res) {
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&rq[i]);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const float2 f = __bfloat1622float2(h2[j]);
+                            v[8 * i + 2 * j] += f.x;
+                            v[8 * i + 2 * j + 1] += f.y;
+                        }
+                    }
+                }
+                if (e_relu && e_aar) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+                }
+                const int sw = (lane >> 1) & 3;  // 64-byte swizzle: 16 B chunk j of row r at r*64 + ((j ^ (r>>1 & 3)) * 16)
+                if (raw) {
+                    // fp32 partials: two 16-column boxes (both 2 KB halves of the slab)
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int hb = 0; hb < 2; ++hb) {
+                        uint8_t* rowp = slab + hb * 2048 + lane * 64;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j)
+                            *reinterpret_cast<float4*>(rowp + ((j ^ sw) << 4)) =
+                                make_float4(v[16 * hb + 4 * j], v[16 * hb + 4 * j + 1], v[16 * hb + 4 * j + 2], v[16 * hb + 4 * j + 3]);
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+#pragma unroll
+                        for (int hb = 0; hb < 2; ++hb)
+                            asm volatile(
+                                "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                                    reinterpret_cast<uint64_t>(&to)),
+                                "r"(col0 + 16 * hb), "r"(row0), "r"(sp), "r"(slab_s + hb * 2048)
+                                : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                } else if (e_geglu) {
+                    // interleaved [16 value | 16 gate] columns -> 16 outputs; 32-byte rows, 32B swizzle
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        v[i] = v[i] * 0.5f * v[16 + i] * (1.f + erff(v[16 + i] * 0.70710678118654752f));
+                    const uint32_t buf = nstore & 1;
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+                    uint8_t* rowp = slab + buf * 2048 + lane * 32;
+                    const int sw2 = (lane >> 2) & 1;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        uint4 o;
+                        o.x = pack_bf16(v[8 * j], v[8 * j + 1]);
+                        o.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+                        o.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+                        o.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+                        *reinterpret_cast<uint4*>(rowp + ((j ^ sw2) << 4)) = o;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                         reinterpret_cast<uint64_t>(&to)),
+                                     "r"(col0 / 2), "r"(row0), "r"(slab_s + buf * 2048)
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    ++nstore;
+                } else {
+                    const uint32_t buf = nstore & 1;
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+                    uint8_t* rowp = slab + buf * 2048 + lane * 64;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint4 o;
+                        o.x = pack_bf16(v[8 * j], v[8 * j + 1]);
+                        o.y = pack_bf16(v[8 * j + 2], v[8 * j + 3]);
+                        o.z = pack_bf16(v[8 * j + 4], v[8 * j + 5]);
+                        o.w = pack_bf16(v[8 * j + 6], v[8 * j + 7]);
+                        *reinterpret_cast<uint4*>(rowp + ((j ^ sw) << 4)) = o;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                                         reinterpret_cast<uint64_t>(&to)),
+                                     "r"(col0), "r"(row0), "r"(slab_s + buf * 2048)
+                                     : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    ++nstore;
+                }
+                if (dstamp) dbg[9 + 3 * (c / 64)] = gtimer();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[5] = gtimer();
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         __syncwarp();
     } else {
         // epilogue warps 2..9 -> TMEM lane quadrant warp % 4 (two warps per quadrant
@@ -285,7 +414,7 @@ __global__ void __launch_bounds__(320, 1)
         const int* e_omap = raw ? nullptr : g.epi.out_img_map;
         const bool e_geglu = !raw && g.epi.geglu;
         const int e_ngn = raw ? 0 : g.epi.n_gn;
-        float* slab = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(tmem_slot) + 16) + (warp - 2) * (32 * 32);
+        float* slab = reinterpret_cast<float*>(slabs + (warp - 2) * 4096);
         uint32_t lt = 0;
         for (int u = blockIdx.x; u < total; u += gridDim.x, ++lt) {
             const int t = u / splits;
@@ -294,6 +423,7 @@ __global__ void __launch_bounds__(320, 1)
             const int m0 = (t / n_tiles) * BM;
             const int n0 = (t % n_tiles) * BN;
             wait_bounded(&tfull[acc], (lt >> 1) & 1);
+            if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[4] = gtimer();
             tc_fence_after();
             const int row = m0 + q * 32 + lane;
             const float* bimg = nullptr;
@@ -304,11 +434,30 @@ __global__ void __launch_bounds__(320, 1)
             const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
             for (int c = half * 32; c < BN; c += 64) {
+                const int col0 = n0 + c;
+                if (col0 >= g.N) continue;  // warp-uniform (columns past N hold no data)
+                // phase-2 geometry: lane -> (row, 8 columns); 4 lanes per row (2 for GEGLU's 16 outputs)
+                const int lpr_shift = e_geglu ? 1 : 2;
+                const int pc = (lane & ((1 << lpr_shift) - 1)) * 8;
+                const int nout = e_geglu ? g.N / 2 : g.N;
+                const int gcol = (e_geglu ? col0 / 2 : col0) + pc;
+                // residual rows of all passes are fetched before the TMEM load so
+                // their latency overlaps the accumulator read-out
+                uint4 resv[4];
+                if (e_res) {
+#pragma unroll
+                    for (int ps = 0; ps < 4; ++ps) {
+                        const int grow = m0 + q * 32 + ps * 8 + (lane >> 2);
+                        resv[ps] = make_uint4(0u, 0u, 0u, 0u);
+                        if (grow < m_eff && gcol + 8 <= nout)
+                            resv[ps] = *reinterpret_cast<const uint4*>(e_res + static_cast<long long>(grow) * e_ldres + gcol);
+                    }
+                }
                 uint32_t r[32];
                 tmem_ld32_nowait(tbase + c, r);
                 tmem_wait_ld();
-                const int col0 = n0 + c;
-                if (col0 >= g.N) continue;  // warp-uniform
+                const bool dstamp = dbg && lt == 0 && warp == 2 && lane == 0;
+                if (dstamp) dbg[7 + 3 * (c / 64)] = gtimer();
                 const bool vec_ok = col0 + 32 <= g.N;
                 float v[32];
 #pragma unroll
@@ -340,12 +489,7 @@ __global__ void __launch_bounds__(320, 1)
                 for (int i = 0; i < 32; i += 4)
                     *reinterpret_cast<float4*>(srow + (((i >> 2) ^ (lane & 7)) << 2)) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
                 __syncwarp();
-                // phase 2: lane -> (row, 8 columns); 4 lanes per row (2 for GEGLU's 16 outputs)
-                const int lpr_shift = e_geglu ? 1 : 2;
-                const int pc = (lane & ((1 << lpr_shift) - 1)) * 8;
-                const int nout = e_geglu ? g.N / 2 : g.N;
-                const int ocol0 = e_geglu ? col0 / 2 : col0;
-                const int gcol = ocol0 + pc;
+                if (dstamp) dbg[8 + 3 * (c / 64)] = gtimer();
                 // GroupNorm partial sums of this lane's 8 columns (<= 2 groups per sink)
                 float ga0 = 0.f, gq0 = 0.f, ga1 = 0.f, gq1 = 0.f, gb0 = 0.f, gr0 = 0.f, gb1 = 0.f, gr1 = 0.f;
                 int gsplit0 = 8, gsplit1 = 8;
@@ -357,9 +501,10 @@ __global__ void __launch_bounds__(320, 1)
                     const int ch0 = g.epi.gn[1].c_off + gcol;
                     gsplit1 = (ch0 / g.epi.gn[1].cg + 1) * g.epi.gn[1].cg - ch0;
                 }
-#pragma unroll 1
-                for (int rr = 0; rr < 32; rr += (32 >> lpr_shift)) {
-                    const int lr = rr + (lane >> lpr_shift);
+#pragma unroll
+                for (int ps = 0; ps < 4; ++ps) {
+                    if (e_geglu && ps >= 2) break;
+                    const int lr = ps * (32 >> lpr_shift) + (lane >> lpr_shift);
                     const int grow = m0 + q * 32 + lr;
                     if (grow >= m_eff || gcol >= nout) continue;
                     const float* sr = slab + lr * 32;
@@ -376,7 +521,7 @@ __global__ void __launch_bounds__(320, 1)
                     if (e_res) {
                         const __nv_bfloat16* rp = e_res + static_cast<long long>(grow) * e_ldres + gcol;
                         if (full8) {
-                            const uint4 rv = *reinterpret_cast<const uint4*>(rp);
+                            const uint4 rv = resv[ps];
                             const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
 #pragma unroll
                             for (int i = 0; i < 8; ++i) w8[i] += __bfloat162float(rb[i]);
@@ -442,6 +587,7 @@ __global__ void __launch_bounds__(320, 1)
                         }
                     }
                 }
+                if (dstamp) dbg[9 + 3 * (c / 64)] = gtimer();
                 // lanes sharing columns (lane bits 2..4) combine; lanes 0..3 add one
                 // fixed-point atomic per (group, moment)
                 if (e_ngn > 0) {
@@ -475,19 +621,26 @@ __global__ void __launch_bounds__(320, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[5] = gtimer();
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (dbg && threadIdx.x == 0) dbg[6] = gtimer();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
 }
 
-// Split-K finish: sum the fp32 partials and apply the full epilogue, 8 columns
-// per thread, coalesced.
-__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, GemmEpilogue e) {
+// Split-K finish: sum the fp32 partials (fixed split order, so the result is
+// deterministic) and apply the full epilogue.  One thread = 8 columns of one
+// row; the partials of up to 4 splits are in flight at once (L2-resident,
+// __ldcg), residual / bias / output are 16-byte vectors.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N,
+                                                            const GemmEpilogue e) {
+    pdl_launch();
+    pdl_wait();
     int m_eff = M;
     if (e.rows_dev) {
         const long long lim = static_cast<long long>(*e.rows_dev) * e.rows_per_unit;
@@ -495,32 +648,69 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
     }
     const int nv = (N + 7) / 8;
     const long long total = static_cast<long long>(m_eff) * nv;
+    const long long plane = static_cast<long long>(M) * N;
+    const bool vec = (N % 8) == 0;
     for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<long long>(gridDim.x) * blockDim.x) {
         const int row = static_cast<int>(idx / nv);
         const int col = static_cast<int>(idx % nv) * 8;
         const int cnt = N - col < 8 ? N - col : 8;
+        const float* base = ws + static_cast<long long>(row) * N + col;
         float w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int sp = 0; sp < splits; ++sp) {
-            const float* p = ws + (static_cast<long long>(sp) * M + row) * N + col;
-            if (cnt == 8 && (N % 4) == 0) {
-                const float4 a = *reinterpret_cast<const float4*>(p);
-                const float4 b = *reinterpret_cast<const float4*>(p + 4);
-                w[0] += a.x; w[1] += a.y; w[2] += a.z; w[3] += a.w;
-                w[4] += b.x; w[5] += b.y; w[6] += b.z; w[7] += b.w;
+        if (vec) {
+            for (int s0 = 0; s0 < splits; s0 += 4) {
+                float4 a[4], b[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (s0 + j < splits) {
+                        a[j] = __ldcg(reinterpret_cast<const float4*>(base + (s0 + j) * plane));
+                        b[j] = __ldcg(reinterpret_cast<const float4*>(base + (s0 + j) * plane + 4));
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (s0 + j < splits) {
+                        w[0] += a[j].x; w[1] += a[j].y; w[2] += a[j].z; w[3] += a[j].w;
+                        w[4] += b[j].x; w[5] += b[j].y; w[6] += b[j].z; w[7] += b[j].w;
+                    }
+                }
+            }
+        } else {
+            for (int sp = 0; sp < splits; ++sp)
+                for (int i = 0; i < cnt; ++i) w[i] += base[sp * plane + i];
+        }
+        float rsd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (e.residual) {
+            const __nv_bfloat16* rp = e.residual + static_cast<long long>(row) * e.ld_res + col;
+            if (cnt == 8 && (e.ld_res % 8) == 0) {
+                const uint4 rv = *reinterpret_cast<const uint4*>(rp);
+                const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&rv);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) rsd[i] = __bfloat162float(rb[i]);
             } else {
-                for (int i = 0; i < cnt; ++i) w[i] += p[i];
+                for (int i = 0; i < cnt; ++i) rsd[i] = __bfloat162float(rp[i]);
+            }
+        }
+        float bs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (e.bias) {
+            if (cnt == 8) {
+                const float4 b0 = *reinterpret_cast<const float4*>(e.bias + col);
+                const float4 b1 = *reinterpret_cast<const float4*>(e.bias + col + 4);
+                bs[0] = b0.x; bs[1] = b0.y; bs[2] = b0.z; bs[3] = b0.w;
+                bs[4] = b1.x; bs[5] = b1.y; bs[6] = b1.z; bs[7] = b1.w;
+            } else {
+                for (int i = 0; i < cnt; ++i) bs[i] = e.bias[col + i];
             }
         }
         const long long im = row / e.rows_per_img;
         const float* bimg = e.bias_img ? e.bias_img + (e.img_index ? e.img_index[im] : im) * (e.bias_img_ld ? e.bias_img_ld : N)
                                        : nullptr;
-        for (int i = 0; i < cnt; ++i) {
-            float x = w[i] * e.scale;
-            if (e.bias) x += e.bias[col + i];
-            if (bimg) x += bimg[col + i];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float x = w[i] * e.scale + bs[i];
+            if (bimg && i < cnt) x += bimg[col + i];
             if (!e.act_after_residual) x = act_fn(x, e.act);
-            if (e.residual) x += __bfloat162float(e.residual[static_cast<long long>(row) * e.ld_res + col + i]);
+            x += rsd[i];
             if (e.act_after_residual) x = act_fn(x, e.act);
             w[i] = x;
         }
@@ -547,15 +737,24 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
         }
         long long orow = row;
         if (e.out_img_map) orow = static_cast<long long>(e.out_img_map[im]) * e.rows_per_img + (row - im * e.rows_per_img);
+        const bool ovec = cnt == 8 && (e.ld_out % 8) == 0;
         if (e.out_f32 == 1) {
             float* op = reinterpret_cast<float*>(e.out) + orow * e.ld_out + col;
-            for (int i = 0; i < cnt; ++i) op[i] = w[i];
+            if (ovec) {
+                *reinterpret_cast<float4*>(op) = make_float4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<float4*>(op + 4) = make_float4(w[4], w[5], w[6], w[7]);
+            } else {
+                for (int i = 0; i < cnt; ++i) op[i] = w[i];
+            }
         } else if (e.out_f32 == 2) {
             uint8_t* op = reinterpret_cast<uint8_t*>(e.out) + orow * e.ld_out + col;
             for (int i = 0; i < cnt; ++i) op[i] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(w[i], 0.f), 1.f) * 255.f));
+        } else if (e.out_f32 == 3) {
+            __half* op = reinterpret_cast<__half*>(e.out) + orow * e.ld_out + col;
+            for (int i = 0; i < cnt; ++i) op[i] = __float2half_rn(w[i]);
         } else {
             __nv_bfloat16* op = reinterpret_cast<__nv_bfloat16*>(e.out) + orow * e.ld_out + col;
-            if (cnt == 8 && (e.ld_out % 8) == 0) {
+            if (ovec) {
                 uint4 o;
                 o.x = pack_bf16(w[0], w[1]);
                 o.y = pack_bf16(w[2], w[3]);
@@ -590,10 +789,11 @@ EncodeTiledFn encode_fn() {
 }
 
 void encode(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-            const cuuint32_t* box, const cuuint32_t* estrides) {
-    const CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims,
-                                   strides_bytes, box, estrides, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            const cuuint32_t* box, const cuuint32_t* estrides,
+            CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+            CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
+    const CUresult r = encode_fn()(m, dt, rank, const_cast<void*>(ptr), dims, strides_bytes, box, estrides,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) raise(SDX_CUDA_ERROR, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
 }
@@ -607,25 +807,6 @@ void encode_2d(CUtensorMap* m, const void* ptr, long long rows, long long cols, 
     encode(m, ptr, 2, dims, strides, box, es);
 }
 
-// Largest UMMA N (multiple of 32, <= 256) that minimises padded columns.
-int pick_bn(int N) {
-    if (N <= 64) return 64;
-    static const int cand[] = {256, 224, 192, 160, 128, 96, 64};
-    int best = 64;
-    long long best_cost = -1;
-    for (int bn : cand) {
-        const long long tiles = (N + bn - 1) / bn;
-        const long long waste = tiles * bn - N;
-        // cost: padded work plus a per-tile overhead (A re-read per N tile)
-        const long long cost = waste * 4 + tiles * 24;
-        if (best_cost < 0 || cost < best_cost) {
-            best_cost = cost;
-            best = bn;
-        }
-    }
-    return best;
-}
-
 template <int BN>
 constexpr int stages_for() {
     return BN >= 192 ? 4 : (BN >= 128 ? 5 : 6);
@@ -633,14 +814,14 @@ constexpr int stages_for() {
 
 template <int BN>
 size_t smem_for() {
-    // stages + barriers (256 B) + 8 epilogue slabs of 32 x 32 fp32
-    return static_cast<size_t>(stages_for<BN>()) * (128 * 64 * 2 + BN * 64 * 2) + 1024 + 256 + 8 * 32 * 32 * 4;
+    // alignment pad + stages + 8 epilogue slabs of 4 KB + barriers (256 B)
+    return 1024 + static_cast<size_t>(stages_for<BN>()) * (128 * 64 * 2 + BN * 64 * 2) + 8 * 4096 + 256;
 }
 
-template <int BN, int AMODE>
+template <int BN, int AMODE, bool FAST>
 void launch_t(const GemmPlan& p, cudaStream_t st) {
     constexpr int S = stages_for<BN>();
-    auto k = gemm_tc_kernel<BN, S, AMODE>;
+    auto k = gemm_tc_kernel<BN, S, AMODE, FAST>;
     static bool attr = false;
     const size_t smem = smem_for<BN>();
     if (!attr) {
@@ -663,68 +844,162 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
     g.epi = p.epi;
     g.splits = p.splits;
     g.ws = p.ws;
+    g.dbg = g_dbg;
     const int units = ((p.N + BN - 1) / BN) * ((p.M + 127) / 128) * p.splits;
     dim3 grid(units < kSmCount ? units : kSmCount);
-    k<<<grid, 320, smem, st>>>(p.ta, p.ta2, p.tb, g);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(k, grid, dim3(320), smem, st, p.ta, p.ta2, p.tb, p.to, g);
     if (p.splits > 1) {
         const long long work = static_cast<long long>(p.M) * ((p.N + 7) / 8);
         long long blocks = (work + 255) / 256;
         if (blocks > 4LL * kSmCount) blocks = 4LL * kSmCount;
-        splitk_reduce_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(p.ws, p.splits, p.M, p.N, p.epi);
-        SDX_LAUNCH_CHECK();
+        launch_pdl(splitk_reduce_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st,
+                   static_cast<const float*>(p.ws), p.splits, p.M, p.N, p.epi);
     }
 }
 
-template <int AMODE>
+template <int AMODE, bool FAST>
 void launch_mode(const GemmPlan& p, cudaStream_t st) {
     switch (p.bn) {
-        case 64: launch_t<64, AMODE>(p, st); break;
-        case 96: launch_t<96, AMODE>(p, st); break;
-        case 128: launch_t<128, AMODE>(p, st); break;
-        case 160: launch_t<160, AMODE>(p, st); break;
-        case 192: launch_t<192, AMODE>(p, st); break;
-        case 224: launch_t<224, AMODE>(p, st); break;
-        default: launch_t<256, AMODE>(p, st); break;
+        case 64: launch_t<64, AMODE, FAST>(p, st); break;
+        case 96: launch_t<96, AMODE, FAST>(p, st); break;
+        case 128: launch_t<128, AMODE, FAST>(p, st); break;
+        case 160: launch_t<160, AMODE, FAST>(p, st); break;
+        case 192: launch_t<192, AMODE, FAST>(p, st); break;
+        case 224: launch_t<224, AMODE, FAST>(p, st); break;
+        default: launch_t<256, AMODE, FAST>(p, st); break;
     }
 }
 
 }  // namespace
 
-// Split-K when the output has too few tiles to fill the SMs and K is long.
-void choose_splits(GemmPlan& p) {
-    const int tiles = ((p.N + p.bn - 1) / p.bn) * ((p.M + 127) / 128);
-    const int nk = p.K / 64;
-    int splits = 1;
-    if (tiles < 100 && nk >= 8 && !p.epi.geglu) {
-        splits = kSmCount / tiles;
-        if (splits > nk / 4) splits = nk / 4;
-        if (splits < 1) splits = 1;
-    }
-    p.splits = splits;
+namespace {
+int g_force_bn = 0, g_force_splits = 0;  // tiling override (kernel benchmarks only)
+}  // namespace
+
+void set_gemm_debug_buffer(unsigned long long* dbg) { g_dbg = dbg; }
+
+void set_gemm_tiling_override(int bn, int splits) {
+    g_force_bn = bn;
+    g_force_splits = splits;
+}
+
+// Tile width BN (UMMA N) and split-K factor from a cost model of the
+// persistent kernel, in SM clocks:
+//   per 64-deep K slice   max(MMA 2*BN, smem fill (128 + BN) rows of 128 B) + barrier round trip
+//   per tile epilogue     output (+ residual) bytes at ~48 B/clk/SM, overlapping the next mainloop
+//   per CTA               ceil(units / 148) x max(mainloop, epilogue) + pipeline fill + last epilogue
+//   split-K               + fp32 partial traffic and the reduce kernel
+double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual) {
+    const long long mt = (M + 127) / 128, nt = (N + bn - 1) / bn;
+    const long long units = mt * nt * splits;
+    const int nk = K / 64;
+    const double nku = static_cast<double>((nk + splits - 1) / splits);
+    const double slice = (2.0 * bn > 128.0 + bn ? 2.0 * bn : 128.0 + bn) + 40.0;
+    const double ml = nku * slice;
+    const double eb = splits > 1 ? 4.0 : out_bytes + (residual ? 2.0 : 0.0);
+    const double epi = 128.0 * bn * eb / 48.0 + 400.0;
+    const double per_cta = static_cast<double>((units + kSmCount - 1) / kSmCount);
+    double t = per_cta * (ml > epi ? ml : epi) + 1500.0 + (ml < epi ? ml : epi);
     if (splits > 1) {
-        float* ws = dev_alloc<float>(static_cast<size_t>(splits) * p.M * p.N);
+        const double bytes = static_cast<double>(M) * N * (4.0 * splits + out_bytes + (residual ? 2.0 : 0.0));
+        t += 3000.0 + bytes / (kSmCount * 32.0);
+    }
+    return t;
+}
+
+void choose_tiling(GemmPlan& p) {
+    static const int cand[] = {64, 96, 128, 160, 192, 224, 256};
+    const int nk = p.K / 64;
+    const int out_bytes = p.epi.out_f32 == 1 ? 4 : (p.epi.out_f32 == 2 ? 1 : 2);
+    const bool res = p.epi.residual != nullptr;
+    int best_bn = 64, best_s = 1;
+    double best = -1.0;
+    for (int bn : cand) {
+        if (p.N <= 64 && bn > 64) break;
+        if (p.epi.geglu && bn % 32 != 0) continue;
+        const int smax = p.epi.geglu ? 1 : (nk / 4 < 16 ? nk / 4 : 16);
+        for (int s = 1; s <= (smax > 1 ? smax : 1); ++s) {
+            const double c = gemm_cost(p.M, p.N, p.K, bn, s, out_bytes, res);
+            if (best < 0 || c < best * 0.999) {
+                best = c;
+                best_bn = bn;
+                best_s = s;
+            }
+        }
+    }
+    if (g_force_bn) best_bn = g_force_bn;
+    if (g_force_splits) best_s = g_force_splits;
+    p.bn = best_bn;
+    p.splits = best_s;
+    if (p.splits > 1) {
+        float* ws = dev_alloc<float>(static_cast<size_t>(p.splits) * p.M * p.N);
         p.ws = ws;
         p.ws_owner = std::shared_ptr<void>(ws, [](void* q) { cudaFree(q); });
     }
 }
 
+namespace {
+bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+}  // namespace
+
+// Streamlined epilogue eligibility + its output tensor map: bf16 output (or
+// split-K fp32 partials), N % 32 == 0, no scatter / GEGLU / fused GN statistics,
+// activation none or ReLU, 16-byte aligned vectors.
+void choose_epilogue(GemmPlan& p) {
+    const GemmEpilogue& e = p.epi;
+    p.fast = false;
+    if (p.N % 32 != 0) return;
+    if (p.splits > 1) {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M),
+                                    static_cast<cuuint64_t>(p.splits)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.N) * 4, static_cast<cuuint64_t>(p.M) * p.N * 4};
+        const cuuint32_t box[3] = {16, 32, 1};
+        const cuuint32_t es[3] = {1, 1, 1};
+        encode(&p.to, p.ws, 3, dims, strides, box, es, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_64B);
+        p.fast = true;
+        return;
+    }
+    if (e.out_f32 != 0 || e.out_img_map || e.n_gn > 0) return;
+    if (e.act != kActNone && e.act != kActRelu) return;
+    if (e.ld_out % 8 != 0 || !aligned16(e.out)) return;
+    if (e.geglu) {
+        if (p.N % 64 != 0 || e.residual || e.bias_img || e.act != kActNone || (e.bias && !aligned16(e.bias))) return;
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.N / 2), static_cast<cuuint64_t>(p.M)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e.ld_out) * 2};
+        const cuuint32_t box[2] = {16, 32};
+        const cuuint32_t es[2] = {1, 1};
+        encode(&p.to, e.out, 2, dims, strides, box, es, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_32B);
+        p.fast = true;
+        return;
+    }
+    if (e.residual && (e.ld_res % 8 != 0 || !aligned16(e.residual))) return;
+    if (e.bias && !aligned16(e.bias)) return;
+    if (e.bias_img && (!aligned16(e.bias_img) || (e.bias_img_ld ? e.bias_img_ld : p.N) % 4 != 0)) return;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e.ld_out) * 2};
+    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t es[2] = {1, 1};
+    encode(&p.to, e.out, 2, dims, strides, box, es, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_64B);
+    p.fast = true;
+}
+
 GemmPlan plan_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
                    const GemmEpilogue& epi) {
     if (K % 64 != 0) raise(SDX_INVALID_ARGUMENT, "gemm: K must be a multiple of 64");
+    if (epi.geglu && epi.residual) raise(SDX_INVALID_ARGUMENT, "gemm: GEGLU epilogue takes no residual");
     GemmPlan p;
     p.amode = kAMatrix;
     p.M = M;
     p.N = N;
     p.K = K;
-    p.bn = pick_bn(N);
-    encode_2d(&p.ta, A, M, K, lda, 128);
-    p.ta2 = p.ta;
-    encode_2d(&p.tb, B, N, K, ldb, p.bn);
     p.epi = epi;
     if (p.epi.ld_out == 0) p.epi.ld_out = N;
     if (p.epi.residual && p.epi.ld_res == 0) p.epi.ld_res = N;
-    choose_splits(p);
+    choose_tiling(p);
+    encode_2d(&p.ta, A, M, K, lda, 128);
+    p.ta2 = p.ta;
+    encode_2d(&p.tb, B, N, K, ldb, p.bn);
+    choose_epilogue(p);
     p.valid = true;
     return p;
 }
@@ -738,14 +1013,14 @@ GemmPlan plan_gemm_concat(const __nv_bfloat16* A1, long long lda1, int K1, const
     p.N = N;
     p.K = K;
     p.K1 = K1;
-    p.bn = pick_bn(N);
-    encode_2d(&p.ta, A1, M, K1, lda1, 128);
-    encode_2d(&p.ta2, A2, M, K - K1, lda2, 128);
-    encode_2d(&p.tb, B, N, K, ldb, p.bn);
     p.epi = epi;
     if (p.epi.ld_out == 0) p.epi.ld_out = N;
     if (p.epi.residual && p.epi.ld_res == 0) p.epi.ld_res = N;
-    choose_splits(p);
+    choose_tiling(p);
+    encode_2d(&p.ta, A1, M, K1, lda1, 128);
+    encode_2d(&p.ta2, A2, M, K - K1, lda2, 128);
+    encode_2d(&p.tb, B, N, K, ldb, p.bn);
+    choose_epilogue(p);
     p.valid = true;
     return p;
 }
@@ -773,7 +1048,10 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
     p.M = imgs * p.Ho * p.Wo;
     p.N = Cout;
     p.K = 9 * Cin;
-    p.bn = pick_bn(Cout);
+    p.epi = epi;
+    if (p.epi.ld_out == 0) p.epi.ld_out = Cout;
+    if (p.epi.residual && p.epi.ld_res == 0) p.epi.ld_res = Cout;
+    choose_tiling(p);
     const cuuint64_t dims[4] = {static_cast<cuuint64_t>(Cin), static_cast<cuuint64_t>(W), static_cast<cuuint64_t>(H),
                                 static_cast<cuuint64_t>(imgs)};
     const cuuint64_t strides[3] = {static_cast<cuuint64_t>(Cin) * 2, static_cast<cuuint64_t>(W) * Cin * 2,
@@ -784,20 +1062,25 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
     encode(&p.ta, x, 4, dims, strides, box, es);
     p.ta2 = p.ta;
     encode_2d(&p.tb, w, Cout, 9LL * Cin, 9LL * Cin, p.bn);
-    p.epi = epi;
-    if (p.epi.ld_out == 0) p.epi.ld_out = Cout;
-    if (p.epi.residual && p.epi.ld_res == 0) p.epi.ld_res = Cout;
-    choose_splits(p);
+    choose_epilogue(p);
     p.valid = true;
     return p;
 }
 
 void run_gemm(const GemmPlan& p, cudaStream_t st) {
     if (!p.valid) raise(SDX_LOGIC_ERROR, "run_gemm: invalid plan");
-    switch (p.amode) {
-        case kAConcat: launch_mode<kAConcat>(p, st); break;
-        case kAConv: launch_mode<kAConv>(p, st); break;
-        default: launch_mode<kAMatrix>(p, st); break;
+    if (p.fast) {
+        switch (p.amode) {
+            case kAConcat: launch_mode<kAConcat, true>(p, st); break;
+            case kAConv: launch_mode<kAConv, true>(p, st); break;
+            default: launch_mode<kAMatrix, true>(p, st); break;
+        }
+    } else {
+        switch (p.amode) {
+            case kAConcat: launch_mode<kAConcat, false>(p, st); break;
+            case kAConv: launch_mode<kAConv, false>(p, st); break;
+            default: launch_mode<kAMatrix, false>(p, st); break;
+        }
     }
 }
 

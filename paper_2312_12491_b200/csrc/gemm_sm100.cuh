@@ -59,6 +59,8 @@ struct GemmEpilogue {
 // A prebuilt launch (tensor maps encoded once; replayable / graph-capturable).
 struct GemmPlan {
     CUtensorMap ta, ta2, tb;
+    CUtensorMap to;                     // output (bf16 [M][ld_out]) or split-K partials (fp32 [splits][M][N]) for TMA stores
+    bool fast = false;                  // streamlined TMA-store epilogue (see gemm_tc_kernel)
     int amode = kAMatrix;
     int M = 0, N = 0, K = 0, K1 = 0;   // K1: split point of the concat source
     int bn = 128;
@@ -83,5 +85,15 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
                       int stride, const GemmEpilogue& epi);
 
 void run_gemm(const GemmPlan& p, cudaStream_t st);
+
+// Forces the tile width / split-K factor of subsequently planned GEMMs (0 = cost
+// model).  Kernel benchmarks only.
+void set_gemm_tiling_override(int bn, int splits);
+// Device buffer [grid][16] that subsequent launches fill with %globaltimer phase
+// stamps per CTA (entry, setup done, first stage landed, first tile committed,
+// epilogue start / end, exit); null disables.  Kernel benchmarks only.
+void set_gemm_debug_buffer(unsigned long long* dbg);
+// Modelled cost (SM clocks) of one tiling; see choose_tiling in gemm_sm100.cu.
+double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual);
 
 }  // namespace sdx

@@ -96,6 +96,75 @@ int sdx_kernel_attention(const void* q, int64_t q_rows_total, int64_t ld_q, int 
     });
 }
 
+struct sdx_gemm_plan {
+    sdx::GemmPlan p;
+};
+
+namespace {
+struct TilingOverride {
+    TilingOverride(int bn, int s) { sdx::set_gemm_tiling_override(bn, s); }
+    ~TilingOverride() { sdx::set_gemm_tiling_override(0, 0); }
+};
+}  // namespace
+
+int sdx_kernel_gemm_plan(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int M, int N, int K,
+                         const float* bias, const void* residual, int act, int out_f32, int force_bn,
+                         int force_splits, sdx_gemm_plan** out) {
+    return kguard([&] {
+        sdx::GemmEpilogue e;
+        e.bias = bias;
+        e.residual = static_cast<const bf16*>(residual);
+        e.act = act;
+        e.out = C;
+        e.out_f32 = out_f32;
+        TilingOverride ov(force_bn, force_splits);
+        auto* h = new sdx_gemm_plan{sdx::plan_gemm(static_cast<const bf16*>(A), lda, static_cast<const bf16*>(B), ldb,
+                                                   M, N, K, e)};
+        *out = h;
+    });
+}
+
+int sdx_kernel_conv3x3_plan(const void* x, int imgs, int H, int W, int Cin, const void* w, int Cout, int stride,
+                            const float* bias, const void* residual, int act, void* out, int out_f32, int force_bn,
+                            int force_splits, sdx_gemm_plan** out_plan) {
+    return kguard([&] {
+        sdx::GemmEpilogue e;
+        e.bias = bias;
+        e.residual = static_cast<const bf16*>(residual);
+        e.act = act;
+        e.out = out;
+        e.out_f32 = out_f32;
+        TilingOverride ov(force_bn, force_splits);
+        *out_plan = new sdx_gemm_plan{sdx::plan_conv3x3(static_cast<const bf16*>(x), imgs, H, W, Cin,
+                                                        static_cast<const bf16*>(w), Cout, stride, e)};
+    });
+}
+
+int sdx_kernel_plan_run(sdx_gemm_plan* p, int iters, void* stream) {
+    return kguard([&] {
+        if (!p) sdx::raise(SDX_INVALID_ARGUMENT, "null plan");
+        for (int i = 0; i < iters; ++i) sdx::run_gemm(p->p, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int sdx_kernel_plan_info(sdx_gemm_plan* p, int* bn, int* splits, double* model_clk) {
+    return kguard([&] {
+        if (!p) sdx::raise(SDX_INVALID_ARGUMENT, "null plan");
+        *bn = p->p.bn;
+        *splits = p->p.splits;
+        const int ob = p->p.epi.out_f32 == 1 ? 4 : (p->p.epi.out_f32 == 2 ? 1 : 2);
+        *model_clk = sdx::gemm_cost(p->p.M, p->p.N, p->p.K, p->p.bn, p->p.splits, ob, p->p.epi.residual != nullptr);
+    });
+}
+
+int sdx_kernel_gemm_debug(void* dbg) {
+    return kguard([&] { sdx::set_gemm_debug_buffer(static_cast<unsigned long long*>(dbg)); });
+}
+
+int sdx_kernel_plan_destroy(sdx_gemm_plan* p) {
+    return kguard([&] { delete p; });
+}
+
 struct sdx_unet {
     sdx::UNet* net;
 };

@@ -33,19 +33,24 @@ __device__ __forceinline__ void store8(bf16* p, const float* v) {
     *reinterpret_cast<uint4*>(p) = u;
 }
 
-__device__ __forceinline__ float silu(float x) { return x / (1.f + __expf(-x)); }
-
 // ---- GroupNorm ----------------------------------------------------------------
 
 // Thread layout of both GroupNorm kernels: blockDim = noct x PY, thread
 // (ox, py) owns channel octet ox (8 channels, <= 2 groups since Ct/32 >= 8) and
-// walks pixels py, py + PY, ...  with 4 independent 16-byte loads in flight.
+// walks the pixels py, py + PY, ... of its block's pixel range, 8 independent
+// 16-byte loads in flight.
 __device__ __forceinline__ const bf16* gn_src(const GnPlan& p, int img, int px, int c) {
     return c < p.C1 ? p.x1 + (static_cast<long long>(img) * p.HW + px) * p.C1 + c
                     : p.x2 + (static_cast<long long>(img) * p.HW + px) * p.C2 + (c - p.C1);
 }
 
-__global__ void gn_stats_kernel(GnPlan p) {
+// Statistics: per block fp32 sums over its pixel range (fixed-order smem
+// reduction), then one 2^-20 fixed-point int64 atomic per (group, moment) into
+// p.acc — integer adds are associative, so the totals are deterministic and no
+// block has to wait for the others.
+__global__ void __launch_bounds__(320) gn_stats_kernel(GnPlan p) {
+    pdl_launch();
+    pdl_wait();
     const int img = blockIdx.y;
     if (p.rows_dev && img >= *p.rows_dev) return;
     const int Ct = p.C1 + p.C2;
@@ -55,23 +60,23 @@ __global__ void gn_stats_kernel(GnPlan p) {
     const int cg = Ct / p.groups;
     const int c = ox * 8;
     const int g0 = c / cg, split = (g0 + 1) * cg - c;
-    const int pp = PY * 8;  // pixels per block
-    const int pix0 = blockIdx.x * pp;
+    const int px0 = blockIdx.x * p.px_per_block;
+    const int px1 = min(p.HW, px0 + p.px_per_block);
     float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
     if (py < PY) {
+        for (int base = px0 + py; base < px1; base += 8 * PY) {
+            float v[8][8];
 #pragma unroll
-        for (int b = 0; b < 2; ++b) {
-            float v[4][8];
-            bool ok[4];
+            for (int k = 0; k < 8; ++k) {
+                const int px = base + k * PY;
+                if (px < px1) load8(gn_src(p, img, px, c), v[k]);
+                else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int px = pix0 + py + (b * 4 + k) * PY;
-                ok[k] = px < p.HW;
-                if (ok[k]) load8(gn_src(p, img, px, c), v[k]);
+                    for (int i = 0; i < 8; ++i) v[k][i] = 0.f;
+                }
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                if (!ok[k]) continue;
+            for (int k = 0; k < 8; ++k) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
                     if (i < split) {
@@ -107,78 +112,45 @@ __global__ void gn_stats_kernel(GnPlan p) {
         float a = 0.f, b = 0.f;
         const int o0 = (g * cg) / 8, o1 = ((g + 1) * cg - 1) / 8;
         for (int o = o0; o <= o1; ++o) {
-            const int oc = o * 8;
-            const int og0 = oc / cg;
+            const int og0 = (o * 8) / cg;
             const int part = og0 == g ? 0 : 2;  // this octet's first or second group
             a += sm[o * 4 + part];
             b += sm[o * 4 + part + 1];
         }
-        float* out = p.partial + ((static_cast<long long>(img) * p.chunks + blockIdx.x) * p.groups + g) * 2;
-        out[0] = a;
-        out[1] = b;
-    }
-    // the last chunk of this image to finish reduces all chunks (fp64, fixed order)
-    __shared__ unsigned int last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) last = atomicAdd(&p.counter[img], 1u) == static_cast<unsigned>(p.chunks - 1);
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int g = warp; g < p.groups; g += nw) {
-        double a = 0.0, b = 0.0;
-        for (int k = lane; k < p.chunks; k += 32) {
-            const float* pr = p.partial + ((static_cast<long long>(img) * p.chunks + k) * p.groups + g) * 2;
-            a += __ldcg(pr);
-            b += __ldcg(pr + 1);
-        }
-        for (int off = 16; off; off >>= 1) {
-            a += __shfl_xor_sync(0xffffffffu, a, off);
-            b += __shfl_xor_sync(0xffffffffu, b, off);
-        }
-        if (lane == 0) {
-            const double n = static_cast<double>(cg) * p.HW;
-            const double mean = a / n;
-            double var = b / n - mean * mean;
-            if (var < 0) var = 0;
-            p.stats[(img * p.groups + g) * 2] = static_cast<float>(mean);
-            p.stats[(img * p.groups + g) * 2 + 1] = static_cast<float>(1.0 / sqrt(var + p.eps));
-        }
-    }
-    if (threadIdx.x == 0) p.counter[img] = 0;
-}
-
-__device__ __forceinline__ void gn_group_stats(const GnPlan& p, int img, int g, float* mean, float* rstd) {
-    if (p.acc) {
-        const int cg = (p.C1 + p.C2) / p.groups;
-        const double inv = 1.0 / 1048576.0;
-        const double n = static_cast<double>(cg) * p.HW;
-        const double m = static_cast<double>(static_cast<long long>(p.acc[(img * p.groups + g) * 2])) * inv / n;
-        double var = static_cast<double>(static_cast<long long>(p.acc[(img * p.groups + g) * 2 + 1])) * inv / n - m * m;
-        if (var < 0) var = 0;
-        *mean = static_cast<float>(m);
-        *rstd = static_cast<float>(1.0 / sqrt(var + p.eps));
-    } else {
-        *mean = p.stats[(img * p.groups + g) * 2];
-        *rstd = p.stats[(img * p.groups + g) * 2 + 1];
+        unsigned long long* acc = p.acc + (static_cast<long long>(img) * p.groups + g) * 2;
+        atomicAdd(acc, static_cast<unsigned long long>(__float2ll_rn(a * 1048576.f)));
+        atomicAdd(acc + 1, static_cast<unsigned long long>(__float2ll_rn(b * 1048576.f)));
     }
 }
 
-__global__ void gn_apply_kernel(GnPlan p) {
+__global__ void __launch_bounds__(320) gn_apply_kernel(GnPlan p) {
+    pdl_launch();
+    pdl_wait();
     const int img = blockIdx.y;
     if (p.rows_dev && img >= *p.rows_dev) return;
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
     const int PY = blockDim.x / noct;
     const int ox = threadIdx.x % noct, py = threadIdx.x / noct;
-    if (py >= PY) return;
     const int cg = Ct / p.groups;
+    // per-image group statistics (fp64 from the fixed-point sums), once per block
+    __shared__ float st[64][2];
+    for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
+        const double inv = 1.0 / 1048576.0;
+        const double n = static_cast<double>(cg) * p.HW;
+        const unsigned long long* acc = p.acc + (static_cast<long long>(img) * p.groups + g) * 2;
+        const double m = static_cast<double>(static_cast<long long>(acc[0])) * inv / n;
+        double var = static_cast<double>(static_cast<long long>(acc[1])) * inv / n - m * m;
+        if (var < 0) var = 0;
+        st[g][0] = static_cast<float>(m);
+        st[g][1] = static_cast<float>(1.0 / sqrt(var + p.eps));
+    }
+    __syncthreads();
+    if (py >= PY) return;
     const int c = ox * 8;
     const int g0 = c / cg, split = (g0 + 1) * cg - c;
-    float m0, r0, m1 = 0.f, r1 = 0.f;
-    gn_group_stats(p, img, g0, &m0, &r0);
-    if (split < 8) gn_group_stats(p, img, g0 + 1, &m1, &r1);
+    const float m0 = st[g0][0], r0 = st[g0][1];
+    const float m1 = split < 8 ? st[g0 + 1][0] : 0.f, r1 = split < 8 ? st[g0 + 1][1] : 0.f;
     float sc[8], sh[8];  // y = x * sc + sh
     {
         const float4 ga = *reinterpret_cast<const float4*>(p.gamma + c), gb = *reinterpret_cast<const float4*>(p.gamma + c + 4);
@@ -192,26 +164,26 @@ __global__ void gn_apply_kernel(GnPlan p) {
             sh[i] = bet[i] - m * r * gam[i];
         }
     }
-    const int pp = PY * 4;
-    const int pix0 = blockIdx.x * pp;
-    float v[4][8];
-    bool ok[4];
+    const int px0 = blockIdx.x * p.px_per_block;
+    const int px1 = min(p.HW, px0 + p.px_per_block);
+    for (int base = px0 + py; base < px1; base += 8 * PY) {
+        float v[8][8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int px = pix0 + py + k * PY;
-        ok[k] = px < p.HW;
-        if (ok[k]) load8(gn_src(p, img, px, c), v[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        if (!ok[k]) continue;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float y = v[k][i] * sc[i] + sh[i];
-            v[k][i] = p.silu ? silu(y) : y;
+        for (int k = 0; k < 8; ++k) {
+            const int px = base + k * PY;
+            if (px < px1) load8(gn_src(p, img, px, c), v[k]);
         }
-        const int px = pix0 + py + k * PY;
-        store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int px = base + k * PY;
+            if (px >= px1) continue;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float y = fmaf(v[k][i], sc[i], sh[i]);
+                v[k][i] = p.silu ? __fdividef(y, 1.f + __expf(-y)) : y;
+            }
+            store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v[k]);
+        }
     }
 }
 
@@ -221,6 +193,8 @@ template <int MAXV>
 __global__ void layernorm_kernel(const bf16* __restrict__ x, int rows, int C, const float* __restrict__ gamma,
                                  const float* __restrict__ beta, float eps, bf16* __restrict__ out,
                                  const int* rows_dev, int rows_per_unit) {
+    pdl_launch();
+    pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     int lim = rows;
@@ -281,6 +255,8 @@ __global__ void layernorm_kernel(const bf16* __restrict__ x, int rows, int C, co
 
 __global__ void geglu_kernel(const bf16* __restrict__ in, int rows, int H, bf16* __restrict__ out,
                              const int* rows_dev, int rows_per_unit) {
+    pdl_launch();
+    pdl_wait();
     int lim = rows;
     if (rows_dev) lim = min(lim, *rows_dev * rows_per_unit);
     const int noct = H / 8;
@@ -302,6 +278,8 @@ __global__ void geglu_kernel(const bf16* __restrict__ in, int rows, int H, bf16*
 
 __global__ void upsample_kernel(const bf16* __restrict__ in, int imgs, int H, int W, int C, bf16* __restrict__ out,
                                 const int* rows_dev) {
+    pdl_launch();
+    pdl_wait();
     int lim = imgs;
     if (rows_dev) lim = min(lim, *rows_dev);
     const int noct = C / 8;
@@ -325,6 +303,8 @@ template <typename T>
 __global__ void im2col_kernel(const T* __restrict__ in, long long img_stride, const int* img_src, int imgs, int H,
                               int W, int C, int Kp, float scale, int tclamp, bf16* __restrict__ out,
                               const int* rows_dev) {
+    pdl_launch();
+    pdl_wait();
     int lim = imgs;
     if (rows_dev) lim = min(lim, *rows_dev);
     const int noct = Kp / 8;
@@ -401,6 +381,8 @@ __global__ void fill_const_kernel(float* p, long long n, float v) {
         p[i] = v;
 }
 __global__ void tanh_clamp_kernel(const float* in, float* out, long long n) {
+    pdl_launch();
+    pdl_wait();
     for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * blockDim.x)
         out[i] = tanhf(in[i] / 3.f) * 3.f;
@@ -416,7 +398,7 @@ unsigned grid_for(long long work, int threads) {
 }  // namespace
 
 GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
-                      const float* beta, int silu_, bf16* out, const int* rows_dev) {
+                      const float* beta, int silu_, bf16* out, const int* rows_dev, unsigned long long* acc) {
     GnPlan p{};
     p.x1 = x1;
     p.x2 = x2;
@@ -431,86 +413,74 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
     p.out = out;
     p.imgs = imgs;
     p.rows_dev = rows_dev;
-    p.acc = nullptr;
+    p.acc = acc;
+    p.stats_fused = 0;
     const int Ct = p.C1 + p.C2;
     if (Ct % 8 != 0 || Ct % p.groups != 0 || (p.C2 && p.C1 % 8 != 0))
         raise(SDX_INVALID_ARGUMENT, "groupnorm: channels must be multiples of 8 and 32");
-    // 8 pixels per thread per stats block (two batches of 4 loads in flight)
+    if (Ct / 8 > 320) raise(SDX_INVALID_ARGUMENT, "groupnorm: more than 2560 channels");
+    if (!acc) raise(SDX_INVALID_ARGUMENT, "groupnorm: statistics arena required");
+    // ~3 blocks per SM over all images, every thread >= 8 pixels
     const int noct = Ct / 8;
     const int PY = noct >= 256 ? 1 : 256 / noct;
-    int chunks = (HW + PY * 8 - 1) / (PY * 8);
-    if (chunks < 1) chunks = 1;
-    p.chunks = chunks;
-    p.partial = dev_alloc<float>(static_cast<size_t>(imgs) * chunks * p.groups * 2);
-    p.stats = dev_alloc<float>(static_cast<size_t>(imgs) * p.groups * 2);
-    p.counter = dev_alloc<unsigned int>(static_cast<size_t>(imgs));
-    SDX_CUDA(cudaMemset(p.counter, 0, sizeof(unsigned int) * imgs));
+    int blocks_per_img = (3 * 148 + imgs - 1) / imgs;
+    int ppb = (HW + blocks_per_img - 1) / blocks_per_img;
+    if (ppb < 8 * PY) ppb = 8 * PY;
+    p.px_per_block = ppb;
+    p.chunks = (HW + ppb - 1) / ppb;
     return p;
 }
 
-void free_groupnorm(GnPlan& p) {
-    dev_free(p.partial);
-    dev_free(p.stats);
-    dev_free(p.counter);
-    p.partial = nullptr;
-}
+void free_groupnorm(GnPlan&) {}
 
 void run_groupnorm(const GnPlan& p, cudaStream_t st) {
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
     const int PY = noct >= 256 ? 1 : 256 / noct;
     const int threads = noct * PY;
-    if (!p.acc) {  // statistics not fused into the producer: standalone pass
-        gn_stats_kernel<<<dim3(p.chunks, p.imgs), threads, static_cast<size_t>(threads) * 4 * sizeof(float), st>>>(p);
-        SDX_LAUNCH_CHECK();
+    if (!p.stats_fused) {  // statistics not accumulated by the producer: standalone pass
+        launch_pdl(gn_stats_kernel, dim3(p.chunks, p.imgs), dim3(threads), static_cast<size_t>(threads) * 4 * sizeof(float), st, p);
     }
-    const int ab = (p.HW + PY * 4 - 1) / (PY * 4);
-    gn_apply_kernel<<<dim3(ab, p.imgs), threads, 0, st>>>(p);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(gn_apply_kernel, dim3(p.chunks, p.imgs), dim3(threads), 0, st, p);
 }
 
 void run_layernorm(const bf16* x, int rows, int C, const float* gamma, const float* beta, float eps, bf16* out,
                    const int* rows_dev, int rows_per_unit, cudaStream_t st) {
     const int noct = C / 8;
     const unsigned blocks = static_cast<unsigned>((rows + 7) / 8);
-    if (noct <= 32) layernorm_kernel<1><<<blocks, 256, 0, st>>>(x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
-    else if (noct <= 64) layernorm_kernel<2><<<blocks, 256, 0, st>>>(x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
-    else if (noct <= 160) layernorm_kernel<5><<<blocks, 256, 0, st>>>(x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
+    if (noct <= 32) launch_pdl(layernorm_kernel<1>, dim3(blocks), dim3(256), 0, st, x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
+    else if (noct <= 64) launch_pdl(layernorm_kernel<2>, dim3(blocks), dim3(256), 0, st, x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
+    else if (noct <= 160) launch_pdl(layernorm_kernel<5>, dim3(blocks), dim3(256), 0, st, x, rows, C, gamma, beta, eps, out, rows_dev, rows_per_unit);
     else raise(SDX_INVALID_ARGUMENT, "layernorm: C too large");
-    SDX_LAUNCH_CHECK();
 }
 
 void run_geglu(const bf16* in, int rows, int H, bf16* out, const int* rows_dev, int rows_per_unit, cudaStream_t st) {
-    geglu_kernel<<<grid_for(static_cast<long long>(rows) * H / 8, 256), 256, 0, st>>>(in, rows, H, out, rows_dev,
-                                                                                       rows_per_unit);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(geglu_kernel, dim3(grid_for(static_cast<long long>(rows) * H / 8, 256)), dim3(256), 0, st, in, rows, H, out,
+               rows_dev, rows_per_unit);
 }
 
 void run_upsample2x(const bf16* in, int imgs, int H, int W, int C, bf16* out, const int* rows_dev, cudaStream_t st) {
-    upsample_kernel<<<grid_for(static_cast<long long>(imgs) * 4 * H * W * C / 8, 256), 256, 0, st>>>(in, imgs, H, W,
-                                                                                                      C, out, rows_dev);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(upsample_kernel, dim3(grid_for(static_cast<long long>(imgs) * 4 * H * W * C / 8, 256)), dim3(256), 0, st,
+               in, imgs, H, W, C, out, rows_dev);
 }
 
 void run_im2col3x3_f32(const float* in, int imgs, int H, int W, int C, int Kp, bf16* out, const int* rows_dev,
                        cudaStream_t st) {
-    im2col_kernel<float><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
-        in, static_cast<long long>(H) * W * C, nullptr, imgs, H, W, C, Kp, 1.f, 0, out, rows_dev);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(im2col_kernel<float>, dim3(grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256)), dim3(256), 0, st,
+               in, static_cast<long long>(H) * W * C, static_cast<const int*>(nullptr), imgs, H, W, C, Kp, 1.f, 0, out,
+               rows_dev);
 }
 
 void run_im2col3x3_f32_gather(const float* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
                               int Kp, int tanh_clamp, bf16* out, const int* rows_dev, cudaStream_t st) {
-    im2col_kernel<float><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
-        in, img_stride, img_src, imgs, H, W, C, Kp, 1.f, tanh_clamp, out, rows_dev);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(im2col_kernel<float>, dim3(grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256)), dim3(256), 0, st,
+               in, img_stride, img_src, imgs, H, W, C, Kp, 1.f, tanh_clamp, out, rows_dev);
 }
 
 void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
                       int Kp, bf16* out, const int* rows_dev, cudaStream_t st) {
-    im2col_kernel<uint8_t><<<grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256), 256, 0, st>>>(
-        in, img_stride, img_src, imgs, H, W, C, Kp, 1.f / 255.f, 0, out, rows_dev);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(im2col_kernel<uint8_t>, dim3(grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256)), dim3(256), 0,
+               st, in, img_stride, img_src, imgs, H, W, C, Kp, 1.f / 255.f, 0, out, rows_dev);
 }
 
 void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStream_t st) {
@@ -544,8 +514,7 @@ void run_interleave_geglu(const bf16* w, const float* b, int H, int K, bf16* wou
 }
 
 void run_tanh_clamp(const float* in, float* out, long long n, cudaStream_t st) {
-    tanh_clamp_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, out, n);
-    SDX_LAUNCH_CHECK();
+    launch_pdl(tanh_clamp_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, in, out, n);
 }
 
 }  // namespace sdx

@@ -20,18 +20,17 @@ struct GnPlan {
     const float *gamma, *beta;
     int silu;
     bf16* out;
-    float* partial;  // [imgs][chunks][groups][2]
-    float* stats;    // [imgs][groups][2] mean, rstd (written by the last stats block per image)
-    unsigned int* counter;  // [imgs] stats blocks finished
-    // fused statistics: sums accumulated by the producing GEMM epilogues (GnSink),
-    // 2^-20 fixed point; null -> the standalone stats kernel runs
-    const unsigned long long* acc;
-    int chunks;
+    // per (image, group) sum and sum of squares, 2^-20 fixed point int64 (exact,
+    // order-independent adds); zeroed by the owner before every forward.  Filled
+    // by gn_stats_kernel, or by the producing GEMM epilogues when stats_fused.
+    unsigned long long* acc;
+    int stats_fused;
+    int px_per_block, chunks;  // pixel range per block (both kernels), blocks per image
     int imgs;
     const int* rows_dev;
 };
 GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
-                      const float* beta, int silu, bf16* out, const int* rows_dev);
+                      const float* beta, int silu, bf16* out, const int* rows_dev, unsigned long long* acc);
 void run_groupnorm(const GnPlan& p, cudaStream_t st);
 void free_groupnorm(GnPlan& p);
 

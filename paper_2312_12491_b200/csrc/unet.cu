@@ -60,21 +60,21 @@ void UNet::gemm_op(const std::string& kind, const GemmPlan& p) {
 
 GnPlan UNet::groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, float eps, const float* g,
                        const float* b, int silu, bf16* out) {
-    GnPlan gp = plan_groupnorm(x1, C1, x2, C2, HW, R_, eps, g, b, silu, out, rows_dev_);
+    const size_t need = static_cast<size_t>(R_) * 32 * 2;
+    if (gn_acc_used_ + need > gn_acc_elems_) raise(SDX_LOGIC_ERROR, "UNet: GroupNorm statistics arena exhausted");
+    unsigned long long* acc = gn_acc_ + gn_acc_used_;
+    gn_acc_used_ += need;
+    GnPlan gp = plan_groupnorm(x1, C1, x2, C2, HW, R_, eps, g, b, silu, out, rows_dev_, acc);
     auto p1 = produced_.find(x1);
     auto p2 = x2 ? produced_.find(x2) : produced_.end();
     const bool fusable = p1 != produced_.end() && p1->second->epi.n_gn < 2 && !p1->second->epi.geglu &&
                          (!x2 || (p2 != produced_.end() && p2->second->epi.n_gn < 2 && !p2->second->epi.geglu));
-    const size_t need = static_cast<size_t>(R_) * gp.groups * 2;
-    // Epilogue-fused statistics measured slower than the standalone stats pass
-    // (atomic traffic in the producers' epilogues); opt in with SDX_GN_FUSE=1.
+    // Epilogue-fused statistics (atomics in the producers' epilogues); opt in with SDX_GN_FUSE=1.
     static const bool enabled = [] {
         const char* v = std::getenv("SDX_GN_FUSE");
         return v && v[0] == '1';
     }();
-    if (enabled && fusable && gn_acc_used_ + need <= gn_acc_elems_) {
-        unsigned long long* acc = gn_acc_ + gn_acc_used_;
-        gn_acc_used_ += need;
+    if (enabled && fusable) {
         const int Ct = C1 + (x2 ? C2 : 0);
         GnSink s;
         s.acc = acc;
@@ -83,11 +83,13 @@ GnPlan UNet::groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, f
         s.hw = HW;
         s.c_off = 0;
         p1->second->epi.gn[p1->second->epi.n_gn++] = s;
+        if (p1->second->splits == 1) p1->second->fast = false;  // GN sinks live in the general epilogue
         if (x2) {
             s.c_off = C1;
             p2->second->epi.gn[p2->second->epi.n_gn++] = s;
+            if (p2->second->splits == 1) p2->second->fast = false;
         }
-        gp.acc = acc;
+        gp.stats_fused = 1;
     }
     return gp;
 }
@@ -471,25 +473,43 @@ void UNet::forward(const int* rows_dev, cudaStream_t st) {
         if (ablate.empty() || ablate.find("," + op.kind + ",") == std::string::npos) op.fn(st);
 }
 
-void UNet::forward_profiled(const int* rows_dev, cudaStream_t st, std::vector<std::pair<std::string, float>>* out) {
-    if (rows_dev) SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_dev, sizeof(int), cudaMemcpyDeviceToDevice, st));
-    else SDX_CUDA(cudaMemcpyAsync(rows_buf_, rows_buf_ + 1, sizeof(int), cudaMemcpyDeviceToDevice, st));
-    SDX_CUDA(cudaMemsetAsync(gn_acc_, 0, gn_acc_used_ * sizeof(unsigned long long), st));
-    std::vector<cudaEvent_t> ev(ops_.size() + 1);
-    for (auto& e : ev) SDX_CUDA(cudaEventCreate(&e));
-    SDX_CUDA(cudaEventRecord(ev[0], st));
-    for (size_t i = 0; i < ops_.size(); ++i) {
-        ops_[i].fn(st);
-        SDX_CUDA(cudaEventRecord(ev[i + 1], st));
-    }
-    SDX_CUDA(cudaEventSynchronize(ev.back()));
+// Per-op device times.  A forward runs first (so every op sees its real
+// inputs in L2); then each op is captured alone, 10 back-to-back repetitions in
+// one CUDA graph, and the graph replay is timed with events (no host launch
+// overhead; consecutive repetitions overlap through PDL like neighbouring ops
+// do in the forward).  Ops that accumulate (GroupNorm statistics) then hold
+// repeated sums — the profile is for timing only.
+void UNet::forward_profiled(const int* rows_dev, cudaStream_t, std::vector<std::pair<std::string, float>>* out) {
+    constexpr int kReps = 10;
+    cudaStream_t cs;
+    SDX_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    SDX_CUDA(cudaEventCreate(&e0));
+    SDX_CUDA(cudaEventCreate(&e1));
+    forward(rows_dev, cs);
+    SDX_CUDA(cudaStreamSynchronize(cs));
     out->clear();
     for (size_t i = 0; i < ops_.size(); ++i) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        SDX_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        for (int r = 0; r < kReps; ++r) ops_[i].fn(cs);
+        SDX_CUDA(cudaStreamEndCapture(cs, &graph));
+        SDX_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        SDX_CUDA(cudaGraphLaunch(exec, cs));
+        SDX_CUDA(cudaEventRecord(e0, cs));
+        SDX_CUDA(cudaGraphLaunch(exec, cs));
+        SDX_CUDA(cudaEventRecord(e1, cs));
+        SDX_CUDA(cudaEventSynchronize(e1));
         float ms = 0.f;
-        SDX_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
-        out->push_back({ops_[i].kind, ms});
+        SDX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        out->push_back({ops_[i].kind, ms / kReps});
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
     }
-    for (auto& e : ev) cudaEventDestroy(e);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(cs);
 }
 
 }  // namespace sdx

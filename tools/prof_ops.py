@@ -11,6 +11,7 @@ sys.path.insert(0, ".")
 from paper_2312_12491_b200 import _lib  # noqa: E402
 
 L = _lib.lib
+L.sdx_kernel_last_error.restype = C.c_char_p
 vp = C.c_void_p
 L.sdx_unet_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.c_uint64, C.c_int, C.POINTER(vp)]
 L.sdx_unet_forward.argtypes = [vp, vp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), vp, vp]
@@ -33,7 +34,8 @@ n = C.c_int()
 acc = collections.defaultdict(lambda: [0, 0.0, 0.0])  # count, ms, flops
 kind_acc = collections.defaultdict(lambda: [0.0, 0.0])
 for _ in range(iters):
-    assert L.sdx_unet_profile_detail(h, rows, cap, labels, flops, ms, C.byref(n)) == 0
+    rc = L.sdx_unet_profile_detail(h, rows, cap, labels, flops, ms, C.byref(n))
+    assert rc == 0, (rc, L.sdx_kernel_last_error())
     for i in range(n.value):
         lab = labels[i].decode()
         a = acc[lab]
