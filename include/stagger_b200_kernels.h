@@ -42,7 +42,8 @@ const char* sdx_kernel_last_error(void);
 
 /* Prebuilt GEMM / conv launches for kernel benchmarks: plan once (tensor maps,
  * split-K workspace), replay `iters` times back to back on `stream`.
- * force_bn / force_splits override the cost-model tiling (0 = model). */
+ * force_bn / force_splits override the cost-model tiling (0 = model; force_bn < 0 =
+ * CTA-pair tile of width -force_bn); plan_info reports a CTA-pair tile as bn < 0. */
 typedef struct sdx_gemm_plan sdx_gemm_plan;
 int sdx_kernel_gemm_plan(const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int M, int N, int K,
                          const float* bias, const void* residual, int act, int out_f32, int force_bn,
@@ -56,6 +57,11 @@ int sdx_kernel_plan_destroy(sdx_gemm_plan* p);
 /* Device u64 buffer [grid][8] for per-CTA %globaltimer phase stamps of the next
  * GEMM launches (NULL disables); see set_gemm_debug_buffer in gemm_sm100.cuh. */
 int sdx_kernel_gemm_debug(void* dbg);
+/* Pipeline probe for kernel experiments (results are wrong): 0 off, 1 = TMA only
+ * (no MMAs), 2 = MMA only (no loads). */
+int sdx_kernel_gemm_probe(int mode);
+/* Same for the attention kernel: 1 = no MMAs, 2 = no softmax exponentials. */
+int sdx_kernel_attention_probe(int mode);
 
 /* The batched UNet denoiser (random-init SD-2.1/SD-turbo topology, bf16
  * weights, fp32 accumulation) used by the pipeline's predict_eps_batch slot.

@@ -29,6 +29,7 @@ namespace {
 
 constexpr int BQ = 128, BKV = 128, HD = 64;
 constexpr uint32_t TILE_BYTES = 128 * 64 * 2;  // one 128-row x 64-col bf16 tile (16 KB)
+constexpr int KVS = 4;  // K/V ring depth: TMA latency (~1-2 us under load) exceeds one block's compute
 
 __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
     const uint32_t a = smem_u32(bar);
@@ -86,17 +87,18 @@ __global__ void __launch_bounds__(320, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sQ = smem;                       // 2 x 16 KB
-    uint8_t* sK = sQ + 2 * TILE_BYTES;        // 2 x 16 KB
-    uint8_t* sV = sK + 2 * TILE_BYTES;        // 2 x 16 KB
-    uint8_t* sP = sV + 2 * TILE_BYTES;        // 2 tiles x 32 KB (two 64-key atoms each)
+    uint8_t* sK = sQ + 2 * TILE_BYTES;        // KVS x 16 KB
+    uint8_t* sV = sK + KVS * TILE_BYTES;      // KVS x 16 KB
+    uint8_t* sP = sV + KVS * TILE_BYTES;      // 2 tiles x 32 KB (two 64-key atoms each)
     uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * TILE_BYTES);
     uint64_t* q_full = bars + 0;
-    uint64_t* kv_full = bars + 1;    // [2]
-    uint64_t* kv_empty = bars + 3;   // [2]
-    uint64_t* s_full = bars + 5;     // [2] per tile
-    uint64_t* p_full = bars + 7;     // [2] per tile
-    uint64_t* pv_done = bars + 9;    // [2] per tile
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 12);
+    uint64_t* kv_full = bars + 1;          // [KVS]
+    uint64_t* kv_empty = kv_full + KVS;    // [KVS]
+    uint64_t* s_full = kv_empty + KVS;     // [2] per tile
+    uint64_t* p_full = s_full + 2;         // [2] per tile
+    uint64_t* pv_done = p_full + 2;        // [2] per tile
+    uint64_t* s_free = pv_done + 2;        // [2] per tile: S read out of TMEM (next S may overwrite it)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkv = (a.kv_len + BKV - 1) / BKV;
@@ -108,12 +110,15 @@ __global__ void __launch_bounds__(320, 1)
         tma_prefetch(&tq);
         tma_prefetch(&tkv);
         mbar_init(q_full, 1);
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < KVS; ++i) {
             mbar_init(&kv_full[i], 1);
             mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
             mbar_init(&p_full[i], 128);
             mbar_init(&pv_done[i], 1);
+            mbar_init(&s_free[i], 4);  // one arrival per softmax warp
         }
         fence_barrier_init();
     }
@@ -133,8 +138,8 @@ __global__ void __launch_bounds__(320, 1)
             tma_load_2d(sQ, &tq, q_full, a.q_col0 + head * HD, q_row0);
             if (has1) tma_load_2d(sQ + TILE_BYTES, &tq, q_full, a.q_col0 + head * HD, q_row0 + BQ);
             for (int j = 0; j < nkv; ++j) {
-                const int b = j & 1;
-                wait_bar(&kv_empty[b], ((j >> 1) & 1) ^ 1);
+                const int b = j % KVS;
+                wait_bar(&kv_empty[b], ((j / KVS) & 1) ^ 1);
                 mbar_expect_tx(&kv_full[b], 2 * TILE_BYTES);
                 tma_load_2d(sK + b * TILE_BYTES, &tkv, &kv_full[b], a.k_col0 + head * HD, kv_row0 + j * BKV);
                 tma_load_2d(sV + b * TILE_BYTES, &tkv, &kv_full[b], a.v_col0 + head * HD, kv_row0 + j * BKV);
@@ -149,16 +154,17 @@ __global__ void __launch_bounds__(320, 1)
             tc_fence_after();
             auto issue_s = [&](int t, int j) {
                 const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ + t * TILE_BYTES));
-                const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + (j & 1) * TILE_BYTES));
+                const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + (j % KVS) * TILE_BYTES));
 #pragma unroll
-                for (int k = 0; k < HD / 16; ++k) umma_f16(tmem + t * 192, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
+                for (int k = 0; k < (a.xmode == 1 ? 0 : HD / 16); ++k)
+                    umma_f16(tmem + t * 192, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
                 umma_commit(&s_full[t]);
             };
             auto issue_pv = [&](int t, int j) {
                 const uint32_t pbase = smem_u32(sP + t * 2 * TILE_BYTES);
-                const uint32_t vbase = smem_u32(sV + (j & 1) * TILE_BYTES);
+                const uint32_t vbase = smem_u32(sV + (j % KVS) * TILE_BYTES);
 #pragma unroll
-                for (int k = 0; k < BKV / 16; ++k) {
+                for (int k = 0; k < (a.xmode == 1 ? 0 : BKV / 16); ++k) {
                     const uint64_t dp = desc_kmajor_sw128(pbase + (k >> 2) * TILE_BYTES) + 2 * (k & 3);
                     const uint64_t dv = desc_mnmajor_sw128(vbase + k * 2048, 0);
                     umma_f16(tmem + t * 192 + 128, dp, dv, idesc_o, (j > 0 || k != 0) ? 1u : 0u);
@@ -168,18 +174,22 @@ __global__ void __launch_bounds__(320, 1)
             wait_bar(&kv_full[0], 0);
             tc_fence_after();
             for (int t = 0; t < ntile; ++t) issue_s(t, 0);
+            // S_t(j+1) is issued as soon as tile t's softmax has read S_t(j) out of TMEM
+            // (s_free), overlapping that softmax's exponentials; PV_t(j) once P_t(j) is in smem.
             for (int j = 0; j < nkv; ++j) {
                 const bool more = j + 1 < nkv;
-                if (more) {
-                    wait_bar(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-                }
+                if (more) wait_bar(&kv_full[(j + 1) % KVS], ((j + 1) / KVS) & 1);
                 for (int t = 0; t < ntile; ++t) {
-                    wait_bar(&p_full[t], j & 1);  // P_t(j) in smem, S_t consumed, O_t rescaled
+                    if (more) {
+                        wait_bar(&s_free[t], j & 1);
+                        tc_fence_after();
+                        issue_s(t, j + 1);
+                    }
+                    wait_bar(&p_full[t], j & 1);  // P_t(j) in smem, O_t rescaled
                     tc_fence_after();
-                    if (more) issue_s(t, j + 1);
                     issue_pv(t, j);
                 }
-                umma_commit(&kv_empty[j & 1]);
+                umma_commit(&kv_empty[j % KVS]);
             }
         }
         __syncwarp();
@@ -203,6 +213,10 @@ __global__ void __launch_bounds__(320, 1)
                 tmem_ld32_nowait(s_addr + 64, sr + 64);
                 tmem_ld32_nowait(s_addr + 96, sr + 96);
                 tmem_wait_ld();
+                // S is in registers: the next QK^T may overwrite the TMEM S buffer
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_free[t]);
                 const int kv_valid = a.kv_len - j * BKV;
                 if (kv_valid < BKV) {  // partial last block: masked keys read as -inf
 #pragma unroll
@@ -244,7 +258,7 @@ __global__ void __launch_bounds__(320, 1)
                 float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 const float nm = -m_used;
 #pragma unroll
-                for (int c = 0; c < BKV; c += 16) {
+                for (int c = 0; c < (a.xmode == 2 ? 0 : BKV); c += 16) {
                     uint32_t pk[8];
 #pragma unroll
                     for (int i = 0; i < 16; i += 2) {
@@ -345,15 +359,22 @@ AttnPlan plan_attention(const __nv_bfloat16* q, long long q_rows_total, long lon
     return p;
 }
 
+namespace {
+int g_attn_xmode = 0;
+}
+void set_attention_probe_mode(int mode) { g_attn_xmode = mode; }
+
 void run_attention(const AttnPlan& p, cudaStream_t st) {
     static bool attr = false;
-    const size_t smem = 10 * TILE_BYTES + 1024 + 256;
+    const size_t smem = (2 + 2 * KVS + 4) * TILE_BYTES + 1024 + 256;
     if (!attr) {
         SDX_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;
     }
     dim3 grid((p.a.q_len + 2 * BQ - 1) / (2 * BQ), p.heads, p.images);
-    launch_pdl(attn_kernel, grid, dim3(320), smem, st, p.tq, p.tkv, p.a);
+    AttnArgs a = p.a;
+    a.xmode = g_attn_xmode;
+    launch_pdl(attn_kernel, grid, dim3(320), smem, st, p.tq, p.tkv, a);
 }
 
 }  // namespace sdx

@@ -17,7 +17,11 @@ struct AttnArgs {
     const int* kv_index;          // image -> KV block (prompt index for cross-attention) or null = image
     const int* rows_dev;          // live image count (device) or null
     float scale;
+    int xmode;                    // experiments only: 1 = no MMAs, 2 = no softmax math (pipeline probes)
 };
+
+// Pipeline probe for kernel experiments (results wrong): 0 off, 1 no MMAs, 2 no softmax math.
+void set_attention_probe_mode(int mode);
 
 struct AttnPlan {
     CUtensorMap tq, tkv;

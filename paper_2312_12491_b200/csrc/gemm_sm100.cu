@@ -27,13 +27,15 @@ using namespace sm100;
 namespace {
 
 unsigned long long* g_dbg = nullptr;  // phase timestamps of the next launches (kernel benchmarks)
+int g_xmode = 0;                      // pipeline probe mode of the next launches (experiments)
 
 struct GemmArgs {
     int M, N, K, K1, amode;
     int Ho, Wo, Cin, stride, Wt, Ht, Nt;
     int splits;   // split-K factor (> 1: raw fp32 partials to ws, epilogue in splitk_reduce)
     float* ws;    // [splits][M][N]
-    unsigned long long* dbg;  // optional per-CTA phase timestamps [grid][8] (kernel benchmarks)
+    unsigned long long* dbg;  // optional per-CTA phase timestamps [grid][16] (kernel benchmarks)
+    int xmode;                // experiments only: 1 = no MMAs issued, 2 = no TMA loads (pipeline probes)
     GemmEpilogue epi;
 };
 
@@ -74,16 +76,63 @@ __device__ __forceinline__ float act_fn(float v, int act) {
     }
 }
 
+// GroupNorm statistics of one 32-row x 32-column epilogue chunk (fast path):
+// per group the sum and sum of squares of the stored (bf16-rounded) values of
+// the warp's 32 rows (one image: rows per image are multiples of 32), reduced
+// over the warp with shuffles, one 2^-20 fixed-point int64 atomic per (group,
+// moment) — exact, order-independent, so deterministic.
+__device__ __forceinline__ void gn_sink_chunk(const GemmEpilogue& e, int ngn, const float* v, int col0, int row0,
+                                              bool live, int lane) {
+    float r[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) r[i] = live ? __bfloat162float(__float2bfloat16(v[i])) : 0.f;
+#pragma unroll 1
+    for (int kk = 0; kk < ngn; ++kk) {
+        const GnSink sk = kk == 0 ? e.gn[0] : e.gn[1];
+        const int c0 = sk.c_off + col0;
+        const int g0 = c0 / sk.cg, g1 = (c0 + 31) / sk.cg;
+        const long long img = row0 / sk.hw;
+#pragma unroll 1
+        for (int gi = g0; gi <= g1; ++gi) {
+            const int lo = gi * sk.cg - c0, hi = lo + sk.cg;
+            float a = 0.f, b = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float x = (i >= lo && i < hi) ? r[i] : 0.f;
+                a += x;
+                b = fmaf(x, x, b);
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                a += __shfl_xor_sync(0xffffffffu, a, off);
+                b += __shfl_xor_sync(0xffffffffu, b, off);
+            }
+            if (lane == 0) {
+                unsigned long long* acc = sk.acc + (img * sk.groups + gi) * 2;
+                atomicAdd(acc, static_cast<unsigned long long>(__float2ll_rn(a * kGnFixedScale)));
+                atomicAdd(acc + 1, static_cast<unsigned long long>(__float2ll_rn(b * kGnFixedScale)));
+            }
+        }
+    }
+}
+
 // Persistent: grid = min(tiles, SMs); tiles in (m, n) order with n fastest so
 // consecutive tiles share the A block in L2.  Two TMEM accumulators let the
 // epilogue of tile i overlap the MMAs of tile i+1.
-template <int BN, int STAGES, int AMODE, bool FAST>
+//
+// PAIR: a cluster of two CTAs on one TPC runs 2-SM MMAs (cta_group::2, M = 256):
+// each CTA stages its own 128 A rows and half of the BN B rows, the leader
+// issues the MMAs, every CTA's TMEM holds its 128 output rows x BN and runs its
+// own epilogue.  Halves the per-SM B traffic (L2 and smem) of a 256 x BN tile.
+template <int BN, int STAGES, int AMODE, bool FAST, bool PAIR>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
                    const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap to, const GemmArgs g) {
+    static_assert(!PAIR || FAST, "CTA-pair GEMM uses the fast epilogue");
     constexpr int BM = 128, BK = 64;
+    constexpr int BNL = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
     constexpr uint32_t A_BYTES = BM * BK * 2;
-    constexpr uint32_t B_BYTES = BN * BK * 2;
+    constexpr uint32_t B_BYTES = BNL * BK * 2;
     constexpr uint32_t TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
 
     if (threadIdx.x == 0) pdl_launch();
@@ -115,13 +164,18 @@ __global__ void __launch_bounds__(320, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], 8);  // one arrival per epilogue warp
+            mbar_init(&tempty[i], PAIR ? 16 : 8);  // one arrival per epilogue warp (of both CTAs)
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, TMEM_COLS);
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    if (warp == 1) {
+        if (PAIR) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+        else tmem_alloc(tmem_slot, TMEM_COLS);
+    }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();  // peer barriers initialised before any cross-CTA signal
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     if (dbg && threadIdx.x == 0) dbg[1] = gtimer();
@@ -134,19 +188,22 @@ __global__ void __launch_bounds__(320, 1)
         if (lim < m_eff) m_eff = static_cast<int>(lim);
     }
     const int n_tiles = (g.N + BN - 1) / BN;
-    const int m_tiles = (m_eff + BM - 1) / BM;  // device-decided batch: only live rows' tiles
+    constexpr int MU = PAIR ? 2 * BM : BM;  // rows per work unit (a CTA pair covers 256)
+    const int m_tiles = (m_eff + MU - 1) / MU;  // device-decided batch: only live rows' tiles
     const int splits = g.splits;
     const int total = m_tiles * n_tiles * splits;  // work units: (tile, K split); CTAs past it idle
+    const int ustart = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int ustep = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
     if (warp == 0) {
         if (lane == 0) {
             const int cblocks = AMODE == kAConv ? g.Cin / BK : 1;
             uint32_t it = 0;
-            for (int u = blockIdx.x; u < total; u += gridDim.x) {
+            for (int u = ustart; u < total; u += ustep) {
                 const int t = u / splits, sp = u - t * splits;
                 const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
-                const int m0 = (t / n_tiles) * BM;
-                const int n0 = (t % n_tiles) * BN;
+                const int m0 = (t / n_tiles) * MU + static_cast<int>(rank) * BM;
+                const int n0 = (t % n_tiles) * BN + static_cast<int>(rank) * BNL;
                 int cn0 = 0, cy0 = 0, cx0 = 0;
                 if (AMODE == kAConv) {
                     const int hw = g.Ho * g.Wo;
@@ -159,29 +216,55 @@ __global__ void __launch_bounds__(320, 1)
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     wait_bounded(&empty[s], ph ^ 1);
-                    mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
                     uint8_t* dA = sA + s * A_BYTES;
+                    int ac0, ac1, ac2 = 0, ac3 = 0;  // A box coordinates
+                    const CUtensorMap* amap = &ta;
                     if (AMODE == kAMatrix) {
-                        tma_load_2d(dA, &ta, &full[s], kb * BK, m0);
+                        ac0 = kb * BK;
+                        ac1 = m0;
                     } else if (AMODE == kAConcat) {
                         const int k1b = g.K1 / BK;
-                        if (kb < k1b) tma_load_2d(dA, &ta, &full[s], kb * BK, m0);
-                        else tma_load_2d(dA, &ta2, &full[s], (kb - k1b) * BK, m0);
+                        if (kb < k1b) {
+                            ac0 = kb * BK;
+                        } else {
+                            ac0 = (kb - k1b) * BK;
+                            amap = &ta2;
+                        }
+                        ac1 = m0;
                     } else {
                         const int tap = kb / cblocks;
                         const int cb = kb - tap * cblocks;
                         const int dy = tap / 3, dx = tap - dy * 3;
-                        tma_load_4d(dA, &ta, &full[s], cb * BK, cx0 * g.stride + dx - 1, cy0 * g.stride + dy - 1, cn0);
+                        ac0 = cb * BK;
+                        ac1 = cx0 * g.stride + dx - 1;
+                        ac2 = cy0 * g.stride + dy - 1;
+                        ac3 = cn0;
                     }
-                    tma_load_2d(sB + s * B_BYTES, &tb, &full[s], kb * BK, n0);
+                    if (g.xmode == 2) {  // probe: skip the loads
+                        if (rank == 0) mbar_arrive(&full[s]);
+                        continue;
+                    }
+                    if constexpr (PAIR) {
+                        // both CTAs' loads complete on the leader's full barrier
+                        const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+                        if (rank == 0) mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+                        if (AMODE == kAConv) tma_load_4d_pair(dA, amap, fb, ac0, ac1, ac2, ac3);
+                        else tma_load_2d_pair(dA, amap, fb, ac0, ac1);
+                        tma_load_2d_pair(sB + s * B_BYTES, &tb, fb, kb * BK, n0);
+                    } else {
+                        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
+                        if (AMODE == kAConv) tma_load_4d(dA, amap, &full[s], ac0, ac1, ac2, ac3);
+                        else tma_load_2d(dA, amap, &full[s], ac0, ac1);
+                        tma_load_2d(sB + s * B_BYTES, &tb, &full[s], kb * BK, n0);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+        if (lane == 0 && rank == 0) {  // CTA pair: only the leader issues the 2-SM MMAs
+            constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN);
             uint32_t it = 0, lt = 0;
-            for (int u = blockIdx.x; u < total; u += gridDim.x, ++lt) {
+            for (int u = ustart; u < total; u += ustep, ++lt) {
                 const int sp = u % splits;
                 const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
                 const uint32_t acc = lt & 1;
@@ -197,11 +280,15 @@ __global__ void __launch_bounds__(320, 1)
                     const uint64_t da = desc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
                     const uint64_t db = desc_kmajor_sw128(smem_u32(sB + s * B_BYTES));
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)  // +32 bytes per K=16 step inside the swizzle atom
-                        umma_f16(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-                    umma_commit(&empty[s]);
+                    for (int k = 0; k < (g.xmode == 1 ? 0 : BK / 16); ++k) {  // +32 B per K=16 step in the swizzle atom
+                        if (PAIR) umma_f16_pair(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                        else umma_f16(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                    }
+                    if (PAIR) umma_commit_pair(&empty[s], 3);
+                    else umma_commit(&empty[s]);
                 }
-                umma_commit(&tfull[acc]);
+                if (PAIR) umma_commit_pair(&tfull[acc], 3);
+                else umma_commit(&tfull[acc]);
                 if (dbg && lt == 0) dbg[3] = gtimer();
             }
         }
@@ -227,15 +314,19 @@ __global__ void __launch_bounds__(320, 1)
         const bool e_relu = !raw && g.epi.act == kActRelu;
         const bool e_aar = !raw && g.epi.act_after_residual;
         const bool e_geglu = !raw && g.epi.geglu;
+        const int e_ngn = raw ? 0 : g.epi.n_gn;
+        const float2* e_lnp = raw ? nullptr : g.epi.ln_part;
+        const float* e_lns = g.epi.ln_s;
+        float2* e_rso = raw ? nullptr : g.epi.row_stats_out;
         uint8_t* slab = slabs + (warp - 2) * 4096;
         const uint32_t slab_s = smem_u32(slab);
         uint32_t nstore = 0;  // bf16 boxes issued by this warp (double-buffered 2 KB halves)
         uint32_t lt = 0;
-        for (int u = blockIdx.x; u < total; u += gridDim.x, ++lt) {
+        for (int u = ustart; u < total; u += ustep, ++lt) {
             const int t = u / splits;
             const int sp = u - t * splits;
             const uint32_t acc = lt & 1;
-            const int m0 = (t / n_tiles) * BM;
+            const int m0 = (t / n_tiles) * MU + static_cast<int>(rank) * BM;
             const int n0 = (t % n_tiles) * BN;
             const int row0 = m0 + q * 32;
             const int row = row0 + lane;
@@ -247,6 +338,23 @@ __global__ void __launch_bounds__(320, 1)
                 const long long im = static_cast<long long>(row) / e_rpi;
                 bimg = e_bimg + (e_imgidx ? e_imgidx[im] : im) * e_bimg_ld;
             }
+            // folded LayerNorm: this row's mean / rstd from the producer's partials
+            float ln_mean = 0.f, ln_rstd = 1.f;
+            if (e_lnp) {
+                float s1 = 0.f, s2 = 0.f;
+                if (row < m_eff) {
+                    for (int pi = 0; pi < g.epi.ln_nparts; ++pi) {
+                        const float2 pv = e_lnp[static_cast<long long>(pi) * g.M + row];
+                        s1 += pv.x;
+                        s2 += pv.y;
+                    }
+                }
+                const float inv_c = 1.f / static_cast<float>(g.epi.ln_C);
+                ln_mean = s1 * inv_c;
+                const float var = fmaxf(s2 * inv_c - ln_mean * ln_mean, 0.f);
+                ln_rstd = rsqrtf(var + g.epi.ln_eps);
+            }
+            float rs_sum = 0.f, rs_sq = 0.f;  // row statistics of this tile's stored values
             const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
             for (int c = half * 32; c < BN; c += 64) {
@@ -260,12 +368,22 @@ __global__ void __launch_bounds__(320, 1)
                 }
                 uint32_t r[32];
                 tmem_ld32_nowait(tbase + c, r);
-                tmem_wait_ld();
+                tmem_wait_ld32(r);
                 const bool dstamp = dbg && lt == 0 && warp == 2 && lane == 0;
                 if (dstamp) dbg[7 + 3 * (c / 64)] = gtimer();
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * e_scale;
+                if (e_lnp) {
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4) {
+                        const float4 sv = *reinterpret_cast<const float4*>(e_lns + col0 + i);
+                        v[i] = ln_rstd * fmaf(-ln_mean, sv.x, v[i]);
+                        v[i + 1] = ln_rstd * fmaf(-ln_mean, sv.y, v[i + 1]);
+                        v[i + 2] = ln_rstd * fmaf(-ln_mean, sv.z, v[i + 2]);
+                        v[i + 3] = ln_rstd * fmaf(-ln_mean, sv.w, v[i + 3]);
+                    }
+                }
                 if (e_bias) {
 #pragma unroll
                     for (int i = 0; i < 32; i += 4) {
@@ -299,6 +417,15 @@ __global__ void __launch_bounds__(320, 1)
                 if (e_relu && e_aar) {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = fmaxf(v[i], 0.f);
+                }
+                if (e_ngn > 0) gn_sink_chunk(g.epi, e_ngn, v, col0, row0, row < m_eff, lane);
+                if (e_rso) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float x = __bfloat162float(__float2bfloat16(v[i]));
+                        rs_sum += x;
+                        rs_sq = fmaf(x, x, rs_sq);
+                    }
                 }
                 const int sw = (lane >> 1) & 3;  // 64-byte swizzle: 16 B chunk j of row r at r*64 + ((j ^ (r>>1 & 3)) * 16)
                 if (raw) {
@@ -381,9 +508,14 @@ __global__ void __launch_bounds__(320, 1)
                 }
                 if (dstamp) dbg[9 + 3 * (c / 64)] = gtimer();
             }
+            if (e_rso && row < m_eff)
+                e_rso[static_cast<long long>(2 * (t % n_tiles) + half) * g.M + row] = make_float2(rs_sum, rs_sq);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));  // the leader's barrier
+                else mbar_arrive(&tempty[acc]);
+            }
             if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[5] = gtimer();
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -626,10 +758,12 @@ __global__ void __launch_bounds__(320, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal it
     if (dbg && threadIdx.x == 0) dbg[6] = gtimer();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tmem, TMEM_COLS);
+        if (PAIR) tmem_dealloc_pair(tmem, TMEM_COLS);
+        else tmem_dealloc(tmem, TMEM_COLS);
     }
 }
 
@@ -807,23 +941,27 @@ void encode_2d(CUtensorMap* m, const void* ptr, long long rows, long long cols, 
     encode(m, ptr, 2, dims, strides, box, es);
 }
 
-template <int BN>
+// smem: 1 KB alignment pad + STAGES x (A 16 KB + B BNL x 128 B) + 8 epilogue slabs of
+// 4 KB + barriers; as many stages (<= 8) as fit in 227 KB.
+template <int BN, bool PAIR>
 constexpr int stages_for() {
-    return BN >= 192 ? 4 : (BN >= 128 ? 5 : 6);
+    constexpr int bnl = PAIR ? BN / 2 : BN;
+    constexpr int st = (232448 - 1024 - 8 * 4096 - 256) / (128 * 64 * 2 + bnl * 64 * 2);
+    return st > 8 ? 8 : st;
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 size_t smem_for() {
-    // alignment pad + stages + 8 epilogue slabs of 4 KB + barriers (256 B)
-    return 1024 + static_cast<size_t>(stages_for<BN>()) * (128 * 64 * 2 + BN * 64 * 2) + 8 * 4096 + 256;
+    constexpr int bnl = PAIR ? BN / 2 : BN;
+    return 1024 + static_cast<size_t>(stages_for<BN, PAIR>()) * (128 * 64 * 2 + bnl * 64 * 2) + 8 * 4096 + 256;
 }
 
-template <int BN, int AMODE, bool FAST>
+template <int BN, int AMODE, bool FAST, bool PAIR>
 void launch_t(const GemmPlan& p, cudaStream_t st) {
-    constexpr int S = stages_for<BN>();
-    auto k = gemm_tc_kernel<BN, S, AMODE, FAST>;
+    constexpr int S = stages_for<BN, PAIR>();
+    auto k = gemm_tc_kernel<BN, S, AMODE, FAST, PAIR>;
     static bool attr = false;
-    const size_t smem = smem_for<BN>();
+    const size_t smem = smem_for<BN, PAIR>();
     if (!attr) {
         SDX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;
@@ -845,9 +983,31 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
     g.splits = p.splits;
     g.ws = p.ws;
     g.dbg = g_dbg;
-    const int units = ((p.N + BN - 1) / BN) * ((p.M + 127) / 128) * p.splits;
-    dim3 grid(units < kSmCount ? units : kSmCount);
-    launch_pdl(k, grid, dim3(320), smem, st, p.ta, p.ta2, p.tb, p.to, g);
+    g.xmode = g_xmode;
+    const int n_tiles = (p.N + BN - 1) / BN;
+    if (PAIR) {
+        const int pairs = ((p.M + 255) / 256) * n_tiles * p.splits;
+        const int np = pairs < kSmCount / 2 ? pairs : kSmCount / 2;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * np);
+        cfg.blockDim = dim3(320);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        SDX_CUDA(cudaLaunchKernelEx(&cfg, k, p.ta, p.ta2, p.tb, p.to, g));
+    } else {
+        const int units = n_tiles * ((p.M + 127) / 128) * p.splits;
+        dim3 grid(units < kSmCount ? units : kSmCount);
+        launch_pdl(k, grid, dim3(320), smem, st, p.ta, p.ta2, p.tb, p.to, g);
+    }
     if (p.splits > 1) {
         const long long work = static_cast<long long>(p.M) * ((p.N + 7) / 8);
         long long blocks = (work + 255) / 256;
@@ -859,28 +1019,42 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
 
 template <int AMODE, bool FAST>
 void launch_mode(const GemmPlan& p, cudaStream_t st) {
+    if constexpr (FAST) {
+        if (p.pair) {
+            switch (p.bn) {
+                case 128: launch_t<128, AMODE, true, true>(p, st); return;
+                case 160: launch_t<160, AMODE, true, true>(p, st); return;
+                case 192: launch_t<192, AMODE, true, true>(p, st); return;
+                case 224: launch_t<224, AMODE, true, true>(p, st); return;
+                case 256: launch_t<256, AMODE, true, true>(p, st); return;
+                default: raise(SDX_LOGIC_ERROR, "gemm: unsupported CTA-pair tile width");
+            }
+        }
+    }
     switch (p.bn) {
-        case 64: launch_t<64, AMODE, FAST>(p, st); break;
-        case 96: launch_t<96, AMODE, FAST>(p, st); break;
-        case 128: launch_t<128, AMODE, FAST>(p, st); break;
-        case 160: launch_t<160, AMODE, FAST>(p, st); break;
-        case 192: launch_t<192, AMODE, FAST>(p, st); break;
-        case 224: launch_t<224, AMODE, FAST>(p, st); break;
-        default: launch_t<256, AMODE, FAST>(p, st); break;
+        case 64: launch_t<64, AMODE, FAST, false>(p, st); break;
+        case 96: launch_t<96, AMODE, FAST, false>(p, st); break;
+        case 128: launch_t<128, AMODE, FAST, false>(p, st); break;
+        case 160: launch_t<160, AMODE, FAST, false>(p, st); break;
+        case 192: launch_t<192, AMODE, FAST, false>(p, st); break;
+        case 224: launch_t<224, AMODE, FAST, false>(p, st); break;
+        default: launch_t<256, AMODE, FAST, false>(p, st); break;
     }
 }
 
 }  // namespace
 
 namespace {
-int g_force_bn = 0, g_force_splits = 0;  // tiling override (kernel benchmarks only)
+int g_force_bn = 0, g_force_splits = 0, g_force_pair = 0;  // tiling override (kernel benchmarks only)
 }  // namespace
 
 void set_gemm_debug_buffer(unsigned long long* dbg) { g_dbg = dbg; }
+void set_gemm_probe_mode(int mode) { g_xmode = mode; }
 
-void set_gemm_tiling_override(int bn, int splits) {
+void set_gemm_tiling_override(int bn, int splits, int pair) {
     g_force_bn = bn;
     g_force_splits = splits;
+    g_force_pair = pair;
 }
 
 // Tile width BN (UMMA N) and split-K factor from a cost model of the
@@ -889,16 +1063,27 @@ void set_gemm_tiling_override(int bn, int splits) {
 //   per tile epilogue     output (+ residual) bytes at ~48 B/clk/SM, overlapping the next mainloop
 //   per CTA               ceil(units / 148) x max(mainloop, epilogue) + pipeline fill + last epilogue
 //   split-K               + fp32 partial traffic and the reduce kernel
-double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual) {
-    const long long mt = (M + 127) / 128, nt = (N + bn - 1) / bn;
+// Tile cost model (SM clocks) of the persistent kernel, calibrated on B200:
+//   per 64-deep K slice  max(MMA 2*BN, smem 2*(128 + BNL)) + barrier round trip, where
+//                        BNL = B rows staged per CTA (BN, or BN/2 for a CTA pair) and every
+//                        staged byte is written by TMA and read by the tensor core through
+//                        the 128 B/clk smem port
+//   per tile epilogue    output (+ residual) bytes at ~16 B/clk/SM, overlapping the next mainloop
+//   per CTA              ceil(units / slots) x max(mainloop, epilogue) + pipeline fill + last epilogue
+//   split-K              + fp32 partial traffic and the reduce kernel
+double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual, bool pair) {
+    const long long mu = pair ? 256 : 128;
+    const long long slots = pair ? kSmCount / 2 : kSmCount;
+    const long long mt = (M + mu - 1) / mu, nt = (N + bn - 1) / bn;
     const long long units = mt * nt * splits;
     const int nk = K / 64;
+    const double bnl = pair ? bn / 2.0 : bn;
     const double nku = static_cast<double>((nk + splits - 1) / splits);
-    const double slice = (2.0 * bn > 128.0 + bn ? 2.0 * bn : 128.0 + bn) + 40.0;
+    const double slice = (2.0 * bn > 2.0 * (128.0 + bnl) ? 2.0 * bn : 2.0 * (128.0 + bnl)) + 40.0;
     const double ml = nku * slice;
     const double eb = splits > 1 ? 4.0 : out_bytes + (residual ? 2.0 : 0.0);
-    const double epi = 128.0 * bn * eb / 48.0 + 400.0;
-    const double per_cta = static_cast<double>((units + kSmCount - 1) / kSmCount);
+    const double epi = 128.0 * bn * eb / 16.0 + 400.0;
+    const double per_cta = static_cast<double>((units + slots - 1) / slots);
     double t = per_cta * (ml > epi ? ml : epi) + 1500.0 + (ml < epi ? ml : epi);
     if (splits > 1) {
         const double bytes = static_cast<double>(M) * N * (4.0 * splits + out_bytes + (residual ? 2.0 : 0.0));
@@ -907,30 +1092,72 @@ double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, b
     return t;
 }
 
+namespace {
+bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+
+// Epilogue the plan can use: 0 general, 1 fast bf16, 2 fast GEGLU, 3 fast split-K partials.
+// Fast: bf16 output (or fp32 partials), N % 32 == 0, no scatter, activation none or
+// ReLU, 16-byte aligned vectors.
+int epilogue_kind(const GemmPlan& p, int splits) {
+    const GemmEpilogue& e = p.epi;
+    if (p.N % 32 != 0) return 0;
+    if (splits > 1) return 3;
+    if (e.out_f32 != 0 || e.out_img_map) return 0;
+    if (e.act != kActNone && e.act != kActRelu) return 0;
+    if (e.ld_out % 8 != 0 || !aligned16(e.out)) return 0;
+    if (e.geglu) {
+        if (p.N % 64 != 0 || e.residual || e.bias_img || e.act != kActNone || (e.bias && !aligned16(e.bias))) return 0;
+        return 2;
+    }
+    if (e.residual && (e.ld_res % 8 != 0 || !aligned16(e.residual))) return 0;
+    if (e.bias && !aligned16(e.bias)) return 0;
+    if (e.bias_img && (!aligned16(e.bias_img) || (e.bias_img_ld ? e.bias_img_ld : p.N) % 4 != 0)) return 0;
+    return 1;
+}
+}  // namespace
+
+// Tile width, split-K factor and CTA pairing from gemm_cost.  CTA pairs need the
+// fast epilogue; GEGLU and LayerNorm-folded GEMMs stay single-pass (no split-K).
 void choose_tiling(GemmPlan& p) {
     static const int cand[] = {64, 96, 128, 160, 192, 224, 256};
     const int nk = p.K / 64;
     const int out_bytes = p.epi.out_f32 == 1 ? 4 : (p.epi.out_f32 == 2 ? 1 : 2);
     const bool res = p.epi.residual != nullptr;
+    const bool single = p.epi.geglu || p.epi.ln_part || p.epi.row_stats_out;
+    static const bool pair_on = [] {
+        const char* v = std::getenv("SDX_GEMM_PAIR");
+        return !(v && v[0] == '0');
+    }();
     int best_bn = 64, best_s = 1;
+    bool best_pair = false;
     double best = -1.0;
-    for (int bn : cand) {
-        if (p.N <= 64 && bn > 64) break;
-        if (p.epi.geglu && bn % 32 != 0) continue;
-        const int smax = p.epi.geglu ? 1 : (nk / 4 < 16 ? nk / 4 : 16);
-        for (int s = 1; s <= (smax > 1 ? smax : 1); ++s) {
-            const double c = gemm_cost(p.M, p.N, p.K, bn, s, out_bytes, res);
-            if (best < 0 || c < best * 0.999) {
-                best = c;
-                best_bn = bn;
-                best_s = s;
+    for (int pr = 0; pr < 2; ++pr) {
+        if (pr && !pair_on) break;
+        for (int bn : cand) {
+            if (p.N <= 64 && bn > 64) break;
+            if (pr && bn < 128) continue;
+            const int smax = single ? 1 : (nk / 4 < 16 ? nk / 4 : 16);
+            for (int s = 1; s <= (smax > 1 ? smax : 1); ++s) {
+                if (pr && epilogue_kind(p, s) == 0) continue;
+                const double c = gemm_cost(p.M, p.N, p.K, bn, s, out_bytes, res, pr != 0);
+                if (best < 0 || c < best * 0.999) {
+                    best = c;
+                    best_bn = bn;
+                    best_s = s;
+                    best_pair = pr != 0;
+                }
             }
         }
     }
-    if (g_force_bn) best_bn = g_force_bn;
+    if (g_force_bn) {
+        best_bn = g_force_bn;
+        best_pair = g_force_pair && best_bn >= 128 && best_bn % 32 == 0;
+    }
     if (g_force_splits) best_s = g_force_splits;
+    if (best_pair && epilogue_kind(p, best_s) == 0) best_pair = false;
     p.bn = best_bn;
     p.splits = best_s;
+    p.pair = best_pair;
     if (p.splits > 1) {
         float* ws = dev_alloc<float>(static_cast<size_t>(p.splits) * p.M * p.N);
         p.ws = ws;
@@ -938,49 +1165,38 @@ void choose_tiling(GemmPlan& p) {
     }
 }
 
-namespace {
-bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
-}  // namespace
-
-// Streamlined epilogue eligibility + its output tensor map: bf16 output (or
-// split-K fp32 partials), N % 32 == 0, no scatter / GEGLU / fused GN statistics,
-// activation none or ReLU, 16-byte aligned vectors.
-void choose_epilogue(GemmPlan& p) {
+// Output tensor map of the fast epilogue (if the plan qualifies).
+void choose_epilogue_impl(GemmPlan& p) {
     const GemmEpilogue& e = p.epi;
-    p.fast = false;
-    if (p.N % 32 != 0) return;
-    if (p.splits > 1) {
+    const int kind = epilogue_kind(p, p.splits);
+    p.fast = kind != 0;
+    if (kind == 3) {
         const cuuint64_t dims[3] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M),
                                     static_cast<cuuint64_t>(p.splits)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(p.N) * 4, static_cast<cuuint64_t>(p.M) * p.N * 4};
         const cuuint32_t box[3] = {16, 32, 1};
         const cuuint32_t es[3] = {1, 1, 1};
         encode(&p.to, p.ws, 3, dims, strides, box, es, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, CU_TENSOR_MAP_SWIZZLE_64B);
-        p.fast = true;
-        return;
-    }
-    if (e.out_f32 != 0 || e.out_img_map || e.n_gn > 0) return;
-    if (e.act != kActNone && e.act != kActRelu) return;
-    if (e.ld_out % 8 != 0 || !aligned16(e.out)) return;
-    if (e.geglu) {
-        if (p.N % 64 != 0 || e.residual || e.bias_img || e.act != kActNone || (e.bias && !aligned16(e.bias))) return;
+    } else if (kind == 2) {
         const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.N / 2), static_cast<cuuint64_t>(p.M)};
         const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e.ld_out) * 2};
         const cuuint32_t box[2] = {16, 32};
         const cuuint32_t es[2] = {1, 1};
         encode(&p.to, e.out, 2, dims, strides, box, es, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_32B);
-        p.fast = true;
-        return;
+    } else if (kind == 1) {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e.ld_out) * 2};
+        const cuuint32_t box[2] = {32, 32};
+        const cuuint32_t es[2] = {1, 1};
+        encode(&p.to, e.out, 2, dims, strides, box, es, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_64B);
     }
-    if (e.residual && (e.ld_res % 8 != 0 || !aligned16(e.residual))) return;
-    if (e.bias && !aligned16(e.bias)) return;
-    if (e.bias_img && (!aligned16(e.bias_img) || (e.bias_img_ld ? e.bias_img_ld : p.N) % 4 != 0)) return;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.N), static_cast<cuuint64_t>(p.M)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e.ld_out) * 2};
-    const cuuint32_t box[2] = {32, 32};
-    const cuuint32_t es[2] = {1, 1};
-    encode(&p.to, e.out, 2, dims, strides, box, es, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, CU_TENSOR_MAP_SWIZZLE_64B);
-    p.fast = true;
+    if (p.pair && !p.fast) raise(SDX_LOGIC_ERROR, "gemm: CTA pair without the fast epilogue");
+}
+
+void choose_epilogue(GemmPlan& p) {
+    choose_epilogue_impl(p);
+    if ((p.epi.ln_part || p.epi.row_stats_out) && !(p.fast && p.splits == 1))
+        raise(SDX_INVALID_ARGUMENT, "gemm: LayerNorm folding needs the fast single-pass epilogue");
 }
 
 GemmPlan plan_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B, long long ldb, int M, int N, int K,
@@ -998,7 +1214,7 @@ GemmPlan plan_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B
     choose_tiling(p);
     encode_2d(&p.ta, A, M, K, lda, 128);
     p.ta2 = p.ta;
-    encode_2d(&p.tb, B, N, K, ldb, p.bn);
+    encode_2d(&p.tb, B, N, K, ldb, p.pair ? p.bn / 2 : p.bn);
     choose_epilogue(p);
     p.valid = true;
     return p;
@@ -1019,7 +1235,7 @@ GemmPlan plan_gemm_concat(const __nv_bfloat16* A1, long long lda1, int K1, const
     choose_tiling(p);
     encode_2d(&p.ta, A1, M, K1, lda1, 128);
     encode_2d(&p.ta2, A2, M, K - K1, lda2, 128);
-    encode_2d(&p.tb, B, N, K, ldb, p.bn);
+    encode_2d(&p.tb, B, N, K, ldb, p.pair ? p.bn / 2 : p.bn);
     choose_epilogue(p);
     p.valid = true;
     return p;
@@ -1061,7 +1277,7 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
     const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(stride), static_cast<cuuint32_t>(stride), 1};
     encode(&p.ta, x, 4, dims, strides, box, es);
     p.ta2 = p.ta;
-    encode_2d(&p.tb, w, Cout, 9LL * Cin, 9LL * Cin, p.bn);
+    encode_2d(&p.tb, w, Cout, 9LL * Cin, 9LL * Cin, p.pair ? p.bn / 2 : p.bn);
     choose_epilogue(p);
     p.valid = true;
     return p;

@@ -54,6 +54,19 @@ struct GemmEpilogue {
     int n_gn = 0;
     const int* rows_dev = nullptr;        // device row-unit count (skip tiles past *rows_dev * rows_per_unit)
     long long rows_per_unit = 0;
+    // LayerNorm folded into this GEMM (fast epilogue only): A holds the raw rows x, B the
+    // folded weights W' = W * gamma, and the epilogue applies
+    //   out = rstd_r * (acc - mean_r * ln_s[n]) + bias[n]      (bias = b + W beta)
+    // with the row statistics summed from ln_nparts partials [ln_nparts][M] (sum, sumsq of
+    // the bf16 A rows) written by the producer of A (row_stats_out below).
+    const float2* ln_part = nullptr;
+    int ln_nparts = 0;
+    int ln_C = 0;
+    float ln_eps = 1e-5f;
+    const float* ln_s = nullptr;
+    // Row statistics of this GEMM's (bf16-rounded) output for a LayerNorm-folded
+    // consumer: [2 * n_tiles][M] float2, one entry per (N tile, epilogue half) per row.
+    float2* row_stats_out = nullptr;
 };
 
 // A prebuilt launch (tensor maps encoded once; replayable / graph-capturable).
@@ -61,6 +74,7 @@ struct GemmPlan {
     CUtensorMap ta, ta2, tb;
     CUtensorMap to;                     // output (bf16 [M][ld_out]) or split-K partials (fp32 [splits][M][N]) for TMA stores
     bool fast = false;                  // streamlined TMA-store epilogue (see gemm_tc_kernel)
+    bool pair = false;                  // CTA-pair 2-SM MMA (M = 256 per pair; needs fast)
     int amode = kAMatrix;
     int M = 0, N = 0, K = 0, K1 = 0;   // K1: split point of the concat source
     int bn = 128;
@@ -88,12 +102,14 @@ void run_gemm(const GemmPlan& p, cudaStream_t st);
 
 // Forces the tile width / split-K factor of subsequently planned GEMMs (0 = cost
 // model).  Kernel benchmarks only.
-void set_gemm_tiling_override(int bn, int splits);
+void set_gemm_tiling_override(int bn, int splits, int pair = 0);
 // Device buffer [grid][16] that subsequent launches fill with %globaltimer phase
 // stamps per CTA (entry, setup done, first stage landed, first tile committed,
 // epilogue start / end, exit); null disables.  Kernel benchmarks only.
 void set_gemm_debug_buffer(unsigned long long* dbg);
+// Pipeline probes (results wrong): 1 = TMA only (no MMAs), 2 = MMA only (no loads).
+void set_gemm_probe_mode(int mode);
 // Modelled cost (SM clocks) of one tiling; see choose_tiling in gemm_sm100.cu.
-double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual);
+double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual, bool pair);
 
 }  // namespace sdx

@@ -102,8 +102,9 @@ struct sdx_gemm_plan {
 
 namespace {
 struct TilingOverride {
-    TilingOverride(int bn, int s) { sdx::set_gemm_tiling_override(bn, s); }
-    ~TilingOverride() { sdx::set_gemm_tiling_override(0, 0); }
+    // bn < 0: CTA-pair tile of width -bn
+    TilingOverride(int bn, int s) { sdx::set_gemm_tiling_override(bn < 0 ? -bn : bn, s, bn < 0 ? 1 : 0); }
+    ~TilingOverride() { sdx::set_gemm_tiling_override(0, 0, 0); }
 };
 }  // namespace
 
@@ -150,15 +151,24 @@ int sdx_kernel_plan_run(sdx_gemm_plan* p, int iters, void* stream) {
 int sdx_kernel_plan_info(sdx_gemm_plan* p, int* bn, int* splits, double* model_clk) {
     return kguard([&] {
         if (!p) sdx::raise(SDX_INVALID_ARGUMENT, "null plan");
-        *bn = p->p.bn;
+        *bn = p->p.pair ? -p->p.bn : p->p.bn;
         *splits = p->p.splits;
         const int ob = p->p.epi.out_f32 == 1 ? 4 : (p->p.epi.out_f32 == 2 ? 1 : 2);
-        *model_clk = sdx::gemm_cost(p->p.M, p->p.N, p->p.K, p->p.bn, p->p.splits, ob, p->p.epi.residual != nullptr);
+        *model_clk = sdx::gemm_cost(p->p.M, p->p.N, p->p.K, p->p.bn, p->p.splits, ob, p->p.epi.residual != nullptr,
+                                    p->p.pair);
     });
 }
 
 int sdx_kernel_gemm_debug(void* dbg) {
     return kguard([&] { sdx::set_gemm_debug_buffer(static_cast<unsigned long long*>(dbg)); });
+}
+
+int sdx_kernel_gemm_probe(int mode) {
+    return kguard([&] { sdx::set_gemm_probe_mode(mode); });
+}
+
+int sdx_kernel_attention_probe(int mode) {
+    return kguard([&] { sdx::set_attention_probe_mode(mode); });
 }
 
 int sdx_kernel_plan_destroy(sdx_gemm_plan* p) {

@@ -508,6 +508,44 @@ __global__ void interleave_geglu_kernel(const bf16* w, const float* b, int H, in
     if (threadIdx.x == 0) bout[r] = b[src];
 }
 
+// LayerNorm folding into the next GEMM: W' = bf16(W * gamma) per input column,
+// s[n] = sum_k W'[n][k] (fp32 of the bf16 values the MMA sees), c[n] = bias[n] +
+// sum_k W[n][k] * beta[k].  One block per output row, fixed-order reductions.
+__global__ void ln_fold_kernel(const bf16* __restrict__ W, int K, const float* __restrict__ gamma,
+                               const float* __restrict__ beta, const float* __restrict__ bias, bf16* __restrict__ Wf,
+                               float* __restrict__ s, float* __restrict__ c) {
+    const int n = blockIdx.x;
+    float a = 0.f, b = 0.f;
+    for (int k = threadIdx.x; k < K; k += blockDim.x) {
+        const float w = __bfloat162float(W[static_cast<long long>(n) * K + k]);
+        const bf16 wf = __float2bfloat16(w * gamma[k]);
+        Wf[static_cast<long long>(n) * K + k] = wf;
+        a += __bfloat162float(wf);
+        b += w * beta[k];
+    }
+    __shared__ float ra[256], rb[256];
+    ra[threadIdx.x] = a;
+    rb[threadIdx.x] = b;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off; off >>= 1) {
+        if (static_cast<int>(threadIdx.x) < off) {
+            ra[threadIdx.x] += ra[threadIdx.x + off];
+            rb[threadIdx.x] += rb[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        s[n] = ra[0];
+        c[n] = (bias ? bias[n] : 0.f) + rb[0];
+    }
+}
+
+void run_ln_fold(const bf16* W, int N, int K, const float* gamma, const float* beta, const float* bias, bf16* Wf,
+                 float* s, float* c, cudaStream_t st) {
+    ln_fold_kernel<<<N, 256, 0, st>>>(W, K, gamma, beta, bias, Wf, s, c);
+    SDX_LAUNCH_CHECK();
+}
+
 void run_interleave_geglu(const bf16* w, const float* b, int H, int K, bf16* wout, float* bout, cudaStream_t st) {
     interleave_geglu_kernel<<<2 * H, 128, 0, st>>>(w, b, H, K, wout, bout);
     SDX_LAUNCH_CHECK();

@@ -66,6 +66,11 @@ void fill_const_f32(float* p, long long n, float v, cudaStream_t st);
 // rows) into 16-row blocks [value 16j.. | gate 16j..] for the fused GEMM epilogue.
 void run_interleave_geglu(const bf16* w, const float* b, int H, int K, bf16* wout, float* bout, cudaStream_t st);
 
+// LayerNorm folded into the following GEMM: Wf = bf16(W * gamma) ([N][K], gamma
+// over K), s[n] = sum_k Wf[n][k], c[n] = bias[n] (or 0) + sum_k W[n][k] * beta[k].
+void run_ln_fold(const bf16* W, int N, int K, const float* gamma, const float* beta, const float* bias, bf16* Wf,
+                 float* s, float* c, cudaStream_t st);
+
 // elementwise: TAESD decoder input clamp  y = tanh(x / 3) * 3  (fp32 -> fp32)
 void run_tanh_clamp(const float* in, float* out, long long n, cudaStream_t st);
 

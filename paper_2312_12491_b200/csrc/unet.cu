@@ -67,9 +67,12 @@ GnPlan UNet::groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, f
     GnPlan gp = plan_groupnorm(x1, C1, x2, C2, HW, R_, eps, g, b, silu, out, rows_dev_, acc);
     auto p1 = produced_.find(x1);
     auto p2 = x2 ? produced_.find(x2) : produced_.end();
-    const bool fusable = p1 != produced_.end() && p1->second->epi.n_gn < 2 && !p1->second->epi.geglu &&
-                         (!x2 || (p2 != produced_.end() && p2->second->epi.n_gn < 2 && !p2->second->epi.geglu));
-    // Epilogue-fused statistics (atomics in the producers' epilogues); opt in with SDX_GN_FUSE=1.
+    // only single-pass fast-epilogue producers (split-K reductions would need per-8-column atomics)
+    auto ok = [](const GemmPlan* q) { return q->epi.n_gn < 2 && !q->epi.geglu && q->fast && q->splits == 1; };
+    const bool fusable = p1 != produced_.end() && ok(p1->second) && (!x2 || (p2 != produced_.end() && ok(p2->second)));
+    // Statistics accumulated in the producers' epilogues instead of a stats pass: opt in
+    // with SDX_GN_FUSE=1 (measured a wash on B200 at 4 rows: the stats kernel it removes
+    // costs about what the epilogue atomics add to these epilogue-bound GEMMs).
     static const bool enabled = [] {
         const char* v = std::getenv("SDX_GN_FUSE");
         return v && v[0] == '1';
@@ -83,11 +86,9 @@ GnPlan UNet::groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, f
         s.hw = HW;
         s.c_off = 0;
         p1->second->epi.gn[p1->second->epi.n_gn++] = s;
-        if (p1->second->splits == 1) p1->second->fast = false;  // GN sinks live in the general epilogue
         if (x2) {
             s.c_off = C1;
             p2->second->epi.gn[p2->second->epi.n_gn++] = s;
-            if (p2->second->splits == 1) p2->second->fast = false;
         }
         gp.stats_fused = 1;
     }
@@ -185,11 +186,49 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
         e.rows_per_unit = HW;
         gemm_op(kind, plan_gemm(a, K, w, K, static_cast<int>(M), N, K, e));
     };
-    auto layernorm = [&](const bf16* in, bf16* out, const std::string& n2) {
-        float* g = wf32(n2 + ".g", {C}, 0.f, 1.f);
-        float* b = wf32(n2 + ".b", {C}, 0.f, 0.f);
+    // LayerNorm -> linear: folded into the GEMM (raw rows as A, W' = W * gamma, row
+    // statistics from the producer's epilogue) when the producer of `in` runs the
+    // single-pass fast epilogue; otherwise a LayerNorm pass into a scratch tensor.
+    // Opt in with SDX_LN_FOLD=1 (measured 0.5% slower at 4 rows: the K=320 consumers are
+    // epilogue-bound and the per-row statistics add to that epilogue).
+    static const bool fold_on = [] {
+        const char* v = std::getenv("SDX_LN_FOLD");
+        return v && v[0] == '1';
+    }();
+    auto ln_gemm = [&](const std::string& kind, const bf16* in, const float* lg, const float* lb, const bf16* w, int N,
+                       const float* bias, GemmEpilogue e) {
+        e.bias = bias;
+        e.rows_dev = rows;
+        e.rows_per_unit = HW;
+        auto it = produced_.find(in);
+        GemmPlan* pp = it == produced_.end() ? nullptr : it->second;
+        if (fold_on && pp && pp->fast && pp->splits == 1 && !pp->epi.geglu && !pp->epi.row_stats_out &&
+            pp->M == static_cast<int>(M) && pp->N == C) {
+            const int nt = (pp->N + pp->bn - 1) / pp->bn;
+            float2* rs = dev_alloc<float2>(static_cast<size_t>(2 * nt) * M);
+            allocs_.push_back(rs);
+            pp->epi.row_stats_out = rs;
+            bf16* wf = act(static_cast<long long>(N) * C);
+            float* sv = actf(N);
+            float* cv = actf(N);
+            run_ln_fold(w, N, C, lg, lb, bias, wf, sv, cv, nullptr);
+            e.ln_part = rs;
+            e.ln_nparts = 2 * nt;
+            e.ln_C = C;
+            e.ln_eps = 1e-5f;
+            e.ln_s = sv;
+            e.bias = cv;
+            gemm_op(kind, plan_gemm(in, C, wf, C, static_cast<int>(M), N, C, e));
+            return;
+        }
+        bf16* n = act(M * C);
         const int Mi = static_cast<int>(M);
-        ops_.push_back(Op{"layernorm", [=](cudaStream_t st) { run_layernorm(in, Mi, C, g, b, 1e-5f, out, rows, HW, st); }});
+        ops_.push_back(Op{"layernorm", [=](cudaStream_t st) { run_layernorm(in, Mi, C, lg, lb, 1e-5f, n, rows, HW, st); }});
+        gemm_op(kind, plan_gemm(n, C, w, C, static_cast<int>(M), N, C, e));
+    };
+    auto ln_params = [&](const std::string& n2, float** g, float** b) {
+        *g = wf32(n2 + ".g", {C}, 0.f, 1.f);
+        *b = wf32(n2 + ".b", {C}, 0.f, 0.f);
     };
     bf16* t = act(M * C);
     {
@@ -202,10 +241,14 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
     bf16* h = act(M * C);
     gemm("linear", t, C, wbf(nm + ".proj_in.w", {C, C}, wstd), C, wf32(nm + ".proj_in.b", {C}, 0.02f, 0.f), nullptr, h);
     // self-attention
-    bf16* n1 = act(M * C);
-    layernorm(h, n1, nm + ".ln1");
+    float *l1g, *l1b;
+    ln_params(nm + ".ln1", &l1g, &l1b);
     bf16* qkv = act(M * 3 * C);
-    gemm("linear", n1, C, wbf(nm + ".attn1.qkv.w", {3 * C, C}, wstd), 3 * C, nullptr, nullptr, qkv);
+    {
+        GemmEpilogue e;
+        e.out = qkv;
+        ln_gemm("linear", h, l1g, l1b, wbf(nm + ".attn1.qkv.w", {3 * C, C}, wstd), 3 * C, nullptr, e);
+    }
     bf16* a1 = act(M * C);
     {
         AttnPlan ap = plan_attention(qkv, M, 3 * C, 0, qkv, M, 3 * C, C, 2 * C, a1, C, 0, R_, heads, HW, HW, HW, HW,
@@ -218,10 +261,14 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
     bf16* h2 = act(M * C);
     gemm("linear", a1, C, wbf(nm + ".attn1.out.w", {C, C}, wstd), C, wf32(nm + ".attn1.out.b", {C}, 0.02f, 0.f), h, h2);
     // cross-attention against the cached per-prompt K/V
-    bf16* n2 = act(M * C);
-    layernorm(h2, n2, nm + ".ln2");
+    float *l2g, *l2b;
+    ln_params(nm + ".ln2", &l2g, &l2b);
     bf16* q = act(M * C);
-    gemm("linear", n2, C, wbf(nm + ".attn2.q.w", {C, C}, wstd), C, nullptr, nullptr, q);
+    {
+        GemmEpilogue e;
+        e.out = q;
+        ln_gemm("linear", h2, l2g, l2b, wbf(nm + ".attn2.q.w", {C, C}, wstd), C, nullptr, e);
+    }
     bf16* wkv = wbf(nm + ".attn2.kv.w", {2 * C, cfg_.ctx_dim}, 1.f / std::sqrt(static_cast<float>(cfg_.ctx_dim)));
     const int P = cfg_.n_prompts;
     bf16* kv = act(static_cast<long long>(P) * cfg_.ctx_len * 2 * C);
@@ -243,8 +290,8 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
     bf16* h3 = act(M * C);
     gemm("linear", a2, C, wbf(nm + ".attn2.out.w", {C, C}, wstd), C, wf32(nm + ".attn2.out.b", {C}, 0.02f, 0.f), h2, h3);
     // GEGLU feed-forward
-    bf16* n3 = act(M * C);
-    layernorm(h3, n3, nm + ".ln3");
+    float *l3g, *l3b;
+    ln_params(nm + ".ln3", &l3g, &l3b);
     bf16* u = act(M * 4 * C);
     {
         // FF1 with GEGLU fused in the epilogue: weights / bias permuted once into
@@ -255,13 +302,10 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
         float* b1i = actf(8LL * C);
         run_interleave_geglu(w1, b1, 4 * C, C, w1i, b1i, nullptr);
         GemmEpilogue e;
-        e.bias = b1i;
         e.geglu = 1;
         e.out = u;
         e.ld_out = 4 * C;
-        e.rows_dev = rows;
-        e.rows_per_unit = HW;
-        gemm_op("linear_geglu", plan_gemm(n3, C, w1i, C, static_cast<int>(M), 8 * C, C, e));
+        ln_gemm("linear_geglu", h3, l3g, l3b, w1i, 8 * C, b1i, e);
     }
     bf16* h4 = act(M * C);
     gemm("linear", u, 4 * C, wbf(nm + ".ff2.w", {C, 4 * C}, 1.f / std::sqrt(4.f * C)), C,

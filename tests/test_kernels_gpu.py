@@ -146,3 +146,69 @@ def test_cross_attention(KA, T, heads):
         refs.append(torch.softmax(qq[i] @ kp.transpose(-1, -2) * 0.125, -1) @ vp_)
     ref = torch.stack(refs).transpose(1, 2).reshape(imgs * T, Cd)
     check(out, ref)
+
+
+@pytest.fixture(scope="module")
+def KP(K):
+    vp, i64 = C.c_void_p, C.c_int64
+    K.sdx_kernel_gemm_plan.argtypes = [vp, i64, vp, i64, vp, C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, C.c_int,
+                                       C.c_int, C.c_int, C.POINTER(vp)]
+    K.sdx_kernel_conv3x3_plan.argtypes = [vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp, vp, C.c_int,
+                                          vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]
+    K.sdx_kernel_plan_run.argtypes = [vp, C.c_int, vp]
+    K.sdx_kernel_plan_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double)]
+    K.sdx_kernel_plan_destroy.argtypes = [vp]
+    return K
+
+
+def run_plan(KP, h):
+    bn, sp, clk = C.c_int(), C.c_int(), C.c_double()
+    assert KP.sdx_kernel_plan_info(h, C.byref(bn), C.byref(sp), C.byref(clk)) == 0
+    assert KP.sdx_kernel_plan_run(h, 1, stream()) == 0, KP.sdx_kernel_last_error()
+    torch.cuda.synchronize()
+    KP.sdx_kernel_plan_destroy(h)
+    return bn.value, sp.value
+
+
+# forced tilings: 1-CTA and CTA-pair (bn < 0, 2-SM tcgen05 MMA), with and without split-K,
+# M not a multiple of the 256-row pair tile, residual / bias / ReLU epilogues
+@pytest.mark.parametrize("shape", [(16384, 320, 320), (1000, 640, 1280), (300, 256, 2560), (4096, 1280, 640)])
+@pytest.mark.parametrize("bn,splits", [(-256, 1), (-160, 1), (-128, 3), (128, 1), (160, 2)])
+@pytest.mark.parametrize("act,res", [(0, 1), (2, 0)])
+def test_gemm_tilings(KP, shape, bn, splits, act, res):
+    M, N, Kd = shape
+    g = torch.Generator(device="cuda").manual_seed(M + N + Kd + abs(bn) + splits)
+    A = torch.randn(M, Kd, device="cuda", generator=g).bfloat16()
+    B = (torch.randn(N, Kd, device="cuda", generator=g) / Kd ** 0.5).bfloat16()
+    bias = torch.randn(N, device="cuda", generator=g)
+    R = torch.randn(M, N, device="cuda", generator=g).bfloat16()
+    out = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+    h = C.c_void_p()
+    assert KP.sdx_kernel_gemm_plan(ptr(A), Kd, ptr(B), Kd, ptr(out), M, N, Kd, ptr(bias), ptr(R) if res else None, act,
+                                   0, bn, splits, C.byref(h)) == 0, KP.sdx_kernel_last_error()
+    got_bn, got_s = run_plan(KP, h)
+    assert (got_bn, got_s) == (bn, splits)
+    ref = A.float() @ B.float().T + bias
+    if act == 2:
+        ref = torch.relu(ref)
+    if res:
+        ref = ref + R.float()
+    check(out, ref)
+
+
+@pytest.mark.parametrize("imgs,H,Cin,Cout,stride,bn,splits", [(4, 64, 320, 320, 1, -160, 1), (3, 32, 640, 640, 1, -256, 1),
+                                                           (4, 16, 1280, 1280, 1, -256, 3), (2, 64, 64, 64, 2, -128, 1),
+                                                           (1, 512, 64, 64, 1, -128, 1)])
+def test_conv3x3_pair(KP, imgs, H, Cin, Cout, stride, bn, splits):
+    g = torch.Generator(device="cuda").manual_seed(H * Cin + Cout + 1)
+    x = torch.randn(imgs, H, H, Cin, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(Cout, 3, 3, Cin, device="cuda", generator=g) / (3 * Cin ** 0.5)).bfloat16()
+    bias = torch.randn(Cout, device="cuda", generator=g)
+    Ho = H // stride
+    out = torch.full((imgs, Ho, Ho, Cout), float("nan"), device="cuda", dtype=torch.bfloat16)
+    h = C.c_void_p()
+    assert KP.sdx_kernel_conv3x3_plan(ptr(x), imgs, H, H, Cin, ptr(w), Cout, stride, ptr(bias), None, 0, ptr(out), 0, bn,
+                                      splits, C.byref(h)) == 0, KP.sdx_kernel_last_error()
+    assert run_plan(KP, h) == (bn, splits)
+    ref = torch.nn.functional.conv2d(x.permute(0, 3, 1, 2).float(), w.permute(0, 3, 1, 2).float(), bias, stride, 1)
+    check(out, ref.permute(0, 2, 3, 1))

@@ -23,7 +23,7 @@ L.sdx_kernel_plan_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int), C
 L.sdx_kernel_plan_destroy.argtypes = [vp]
 L.sdx_kernel_last_error.restype = C.c_char_p
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-BNS = [64, 96, 128, 160, 192, 224, 256]
+BNS = [64, 96, 128, 160, 192, 224, 256, -128, -160, -192, -224, -256]  # < 0: CTA pair
 SPLITS = [1, 2, 3, 4, 6, 8, 12, 16]
 
 
@@ -63,7 +63,7 @@ def sweep(label, make, flops, N, K):
     L.sdx_kernel_plan_destroy(h)
     best = (tm, mbn, ms)
     for bn in BNS:
-        if N <= 64 and bn > 64:
+        if N <= 64 and abs(bn) > 64:
             continue
         for s in SPLITS:
             if s > 1 and s > (K // 64) // 4:
