@@ -1087,7 +1087,7 @@ double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, b
     double t = per_cta * (ml > epi ? ml : epi) + 1500.0 + (ml < epi ? ml : epi);
     if (splits > 1) {
         const double bytes = static_cast<double>(M) * N * (4.0 * splits + out_bytes + (residual ? 2.0 : 0.0));
-        t += 3000.0 + bytes / (kSmCount * 32.0);
+        t += 5000.0 + bytes / (kSmCount * 16.0);
     }
     return t;
 }
@@ -1139,6 +1139,10 @@ void choose_tiling(GemmPlan& p) {
             const int smax = single ? 1 : (nk / 4 < 16 ? nk / 4 : 16);
             for (int s = 1; s <= (smax > 1 ? smax : 1); ++s) {
                 if (pr && epilogue_kind(p, s) == 0) continue;
+                // CTA pairs only for long-K layers: measured on the UNet shapes (tools/gemm_sweep.py)
+                // they win for K >= 11520 (1280+ input channels of a 3x3 conv) and lose 10-20%
+                // below that (cluster launch / sync overheads outweigh the halved B traffic)
+                if (pr && p.K < 11520) continue;
                 const double c = gemm_cost(p.M, p.N, p.K, bn, s, out_bytes, res, pr != 0);
                 if (best < 0 || c < best * 0.999) {
                     best = c;
