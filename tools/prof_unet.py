@@ -16,6 +16,15 @@ h = vp()
 assert L.sdx_unet_create(rows, taus, 4, 1234, 0, C.byref(h)) == 0
 steps = (C.c_int * rows)(*[i % 4 for i in range(rows)])
 prompts = (C.c_int * rows)(*[0] * rows)
-for _ in range(iters):
+L.sdx_profiler_start.restype = C.c_int
+L.sdx_profiler_stop.restype = C.c_int
+for i in range(iters):
+    if i == iters - 1:  # ncu --profile-from-start off captures the last forward only
+        L.sdx_memcpy_d2d.restype = C.c_int
+        import torch  # noqa: F401  (sync helper)
+        torch.cuda.synchronize()
+        L.sdx_profiler_start()
     assert L.sdx_unet_forward(h, None, rows, steps, prompts, None, None) == 0
+torch.cuda.synchronize()
+L.sdx_profiler_stop()
 print("ok")
