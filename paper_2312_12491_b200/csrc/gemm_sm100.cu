@@ -131,7 +131,11 @@ __global__ void __launch_bounds__(320, 1)
     static_assert(!PAIR || FAST, "CTA-pair GEMM uses the fast epilogue");
     constexpr int BM = 128, BK = 64;
     constexpr int BNL = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
-    constexpr uint32_t A_BYTES = BM * BK * 2;
+    constexpr bool HALO = AMODE == kAHalo;
+    // halo mode: an A stage is one 3 x 130-pixel x 64-channel box (1024-aligned), B (9 taps x BN
+    // rows) stays resident for the whole kernel
+    constexpr uint32_t HALO_TX = 3 * 130 * 128;
+    constexpr uint32_t A_BYTES = HALO ? ((HALO_TX + 1023) / 1024) * 1024 : BM * BK * 2;
     constexpr uint32_t B_BYTES = BNL * BK * 2;
     constexpr uint32_t TMEM_COLS = (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
 
@@ -140,12 +144,13 @@ __global__ void __launch_bounds__(320, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint8_t* slabs = sB + STAGES * B_BYTES;  // 8 epilogue warps x 4 KB (1024-aligned)
+    uint8_t* slabs = sB + (HALO ? 9 : STAGES) * B_BYTES;  // 8 epilogue warps x 4 KB (1024-aligned)
     uint64_t* full = reinterpret_cast<uint64_t*>(slabs + 8 * 4096);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;   // [2]
     uint64_t* tempty = tfull + 2;       // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* bfull = tempty + 2;       // halo mode: resident B landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(320, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
+        mbar_init(bfull, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
             mbar_init(&tempty[i], PAIR ? 16 : 8);  // one arrival per epilogue warp (of both CTAs)
@@ -195,7 +201,55 @@ __global__ void __launch_bounds__(320, 1)
     const int ustart = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
     const int ustep = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
 
-    if (warp == 0) {
+    if (HALO && warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(bfull, 9 * B_BYTES);
+            for (int tap = 0; tap < 9; ++tap) tma_load_2d(sB + tap * B_BYTES, &tb, bfull, tap * BK, 0);
+            uint32_t it = 0;
+            const int hw = g.Ho * g.Wo;
+            for (int u = ustart; u < total; u += ustep, ++it) {
+                const int m0 = u * BM;  // n_tiles == splits == 1
+                const int cn0 = m0 / hw;
+                const int rem = m0 - cn0 * hw;
+                const int cy0 = rem / g.Wo, cx0 = rem - cy0 * g.Wo;
+                const int s = it % STAGES;
+                wait_bounded(&empty[s], ((it / STAGES) & 1) ^ 1);
+                mbar_expect_tx(&full[s], HALO_TX);
+                tma_load_4d(sA + s * A_BYTES, &ta, &full[s], 0, cx0 - 1, cy0 - 1, cn0);
+            }
+        }
+    } else if (HALO && warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = idesc_bf16(BM, BN);
+            wait_bounded(bfull, 0);
+            uint32_t it = 0;
+            for (int u = ustart; u < total; u += ustep, ++it) {
+                const uint32_t acc = it & 1;
+                wait_bounded(&tempty[acc], ((it >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dtm = tmem + acc * BN;
+                const int s = it % STAGES;
+                wait_bounded(&full[s], (it / STAGES) & 1);
+                tc_fence_after();
+                const uint32_t abase = smem_u32(sA + s * A_BYTES);
+#pragma unroll 1
+                for (int tap = 0; tap < 9; ++tap) {
+                    const int dy = tap / 3, dx = tap - dy * 3;
+                    // output pixel i of the tile reads halo pixel (dy, i + dx): 128 consecutive rows
+                    // the SW128 XOR pattern follows the absolute smem address bits (as the TMA wrote
+                    // it), so a start at any 128-byte row needs no descriptor base offset
+                    const uint64_t da = desc_kmajor_sw128(abase + static_cast<uint32_t>(dy * 130 + dx) * 128);
+                    const uint64_t db = desc_kmajor_sw128(smem_u32(sB + tap * B_BYTES));
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k)
+                        umma_f16(dtm, da + 2 * k, db + 2 * k, idesc, (tap != 0 || k != 0) ? 1u : 0u);
+                }
+                umma_commit(&empty[s]);
+                umma_commit(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else if (warp == 0) {
         if (lane == 0) {
             const int cblocks = AMODE == kAConv ? g.Cin / BK : 1;
             uint32_t it = 0;
@@ -943,25 +997,27 @@ void encode_2d(CUtensorMap* m, const void* ptr, long long rows, long long cols, 
 
 // smem: 1 KB alignment pad + STAGES x (A 16 KB + B BNL x 128 B) + 8 epilogue slabs of
 // 4 KB + barriers; as many stages (<= 8) as fit in 227 KB.
-template <int BN, bool PAIR>
+template <int BN, bool PAIR, int AMODE>
 constexpr int stages_for() {
+    if (AMODE == kAHalo) return 2;  // 2 x 49 KB halo boxes next to 72 KB of resident weights
     constexpr int bnl = PAIR ? BN / 2 : BN;
     constexpr int st = (232448 - 1024 - 8 * 4096 - 256) / (128 * 64 * 2 + bnl * 64 * 2);
     return st > 8 ? 8 : st;
 }
 
-template <int BN, bool PAIR>
+template <int BN, bool PAIR, int AMODE>
 size_t smem_for() {
+    if (AMODE == kAHalo) return 1024 + 2 * 50176 + 9 * BN * 64 * 2 + 8 * 4096 + 256;
     constexpr int bnl = PAIR ? BN / 2 : BN;
-    return 1024 + static_cast<size_t>(stages_for<BN, PAIR>()) * (128 * 64 * 2 + bnl * 64 * 2) + 8 * 4096 + 256;
+    return 1024 + static_cast<size_t>(stages_for<BN, PAIR, AMODE>()) * (128 * 64 * 2 + bnl * 64 * 2) + 8 * 4096 + 256;
 }
 
 template <int BN, int AMODE, bool FAST, bool PAIR>
 void launch_t(const GemmPlan& p, cudaStream_t st) {
-    constexpr int S = stages_for<BN, PAIR>();
+    constexpr int S = stages_for<BN, PAIR, AMODE>();
     auto k = gemm_tc_kernel<BN, S, AMODE, FAST, PAIR>;
     static bool attr = false;
-    const size_t smem = smem_for<BN, PAIR>();
+    const size_t smem = smem_for<BN, PAIR, AMODE>();
     if (!attr) {
         SDX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;
@@ -1283,12 +1339,35 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
     p.ta2 = p.ta;
     encode_2d(&p.tb, w, Cout, 9LL * Cin, 9LL * Cin, p.pair ? p.bn / 2 : p.bn);
     choose_epilogue(p);
+    static const bool halo_on = [] {
+        const char* v = std::getenv("SDX_CONV_HALO");
+        return !(v && v[0] == '0');
+    }();
+    if (halo_on && Cin == 64 && Cout == 64 && stride == 1 && W % 128 == 0 && p.fast && !p.epi.ln_part &&
+        !p.epi.row_stats_out && g_force_bn == 0) {
+        // halo-tiled: 128-pixel row segments, one 3 x 130 x 64 box per tile, resident weights
+        p.amode = kAHalo;
+        p.bn = 64;
+        p.splits = 1;
+        p.pair = false;
+        p.ws = nullptr;
+        p.ws_owner.reset();
+        const cuuint32_t hbox[4] = {64, 130, 3, 1};
+        const cuuint32_t hes[4] = {1, 1, 1, 1};
+        encode(&p.ta, x, 4, dims, strides, hbox, hes);
+        encode_2d(&p.tb, w, Cout, 9LL * Cin, 9LL * Cin, 64);
+        choose_epilogue(p);
+    }
     p.valid = true;
     return p;
 }
 
 void run_gemm(const GemmPlan& p, cudaStream_t st) {
     if (!p.valid) raise(SDX_LOGIC_ERROR, "run_gemm: invalid plan");
+    if (p.amode == kAHalo) {
+        launch_t<64, kAHalo, true, false>(p, st);
+        return;
+    }
     if (p.fast) {
         switch (p.amode) {
             case kAConcat: launch_mode<kAConcat, true>(p, st); break;

@@ -19,7 +19,7 @@
 namespace sdx {
 
 enum { kActNone = 0, kActSilu = 1, kActRelu = 2, kActGelu = 3 };
-enum { kAMatrix = 0, kAConcat = 1, kAConv = 2 };
+enum { kAMatrix = 0, kAConcat = 1, kAConv = 2, kAHalo = 3 };
 
 // GroupNorm statistics accumulated in the epilogue of the GEMM that produces
 // the normalised tensor: per (image, group) sum and sum of squares of the
@@ -94,7 +94,10 @@ GemmPlan plan_gemm(const __nv_bfloat16* A, long long lda, const __nv_bfloat16* B
 GemmPlan plan_gemm_concat(const __nv_bfloat16* A1, long long lda1, int K1, const __nv_bfloat16* A2, long long lda2,
                           const __nv_bfloat16* B, long long ldb, int M, int N, int K, const GemmEpilogue& epi);
 // 3x3 conv, pad 1, stride 1 or 2: x NHWC [imgs][H][W][Cin] bf16, w [Cout][3][3][Cin] bf16,
-// out NHWC [imgs][Ho][Wo][Cout].  Cin % 64 == 0.
+// out NHWC [imgs][Ho][Wo][Cout].  Cin % 64 == 0.  64 -> 64 channel stride-1 convs on rows of
+// >= 128 pixels (the TAESD trunk) run halo-tiled: one 3 x 130-pixel TMA box per 128-pixel output
+// tile feeds all nine taps (UMMA descriptors at 128-byte pixel-row offsets) against
+// weights resident in smem (SDX_CONV_HALO=0 disables).
 GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, const __nv_bfloat16* w, int Cout,
                       int stride, const GemmEpilogue& epi);
 

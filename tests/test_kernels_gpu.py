@@ -212,3 +212,27 @@ def test_conv3x3_pair(KP, imgs, H, Cin, Cout, stride, bn, splits):
     assert run_plan(KP, h) == (bn, splits)
     ref = torch.nn.functional.conv2d(x.permute(0, 3, 1, 2).float(), w.permute(0, 3, 1, 2).float(), bias, stride, 1)
     check(out, ref.permute(0, 2, 3, 1))
+
+
+# halo-tiled 64 -> 64 conv (TAESD trunk): one 3 x 130-pixel box per 128-pixel tile, nine taps
+# as UMMA descriptor offsets, resident weights; bias + residual + ReLU epilogue as TAESD uses it
+@pytest.mark.parametrize("imgs,H,W", [(1, 128, 128), (2, 256, 256), (1, 512, 512), (3, 64, 256)])
+@pytest.mark.parametrize("act,res", [(2, 1), (0, 0)])
+def test_conv3x3_halo(K, imgs, H, W, act, res):
+    g = torch.Generator(device="cuda").manual_seed(H * W + imgs + act)
+    x = torch.randn(imgs, H, W, 64, device="cuda", generator=g).bfloat16()
+    w = (torch.randn(64, 3, 3, 64, device="cuda", generator=g) / 24).bfloat16()
+    bias = torch.randn(64, device="cuda", generator=g)
+    R = torch.randn(imgs, H, W, 64, device="cuda", generator=g).bfloat16()
+    out = torch.full((imgs, H, W, 64), float("nan"), device="cuda", dtype=torch.bfloat16)
+    st = K.sdx_kernel_conv3x3(ptr(x), imgs, H, W, 64, ptr(w), 64, 1, ptr(bias), None, ptr(R) if res else None, act,
+                              ptr(out), 0, stream())
+    assert st == 0, K.sdx_kernel_last_error()
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.conv2d(x.permute(0, 3, 1, 2).float(), w.permute(0, 3, 1, 2).float(), bias, 1, 1)
+    ref = ref.permute(0, 2, 3, 1)
+    if act == 2:
+        ref = torch.relu(ref)  # the kernel-level entry applies the activation before the residual
+    if res:
+        ref = ref + R.float()
+    check(out, ref)

@@ -113,7 +113,7 @@ def conv_case(imgs, H, Cin, Cout, stride=1):
 
 
 def main():
-    rows_list = [int(a) for a in sys.argv[1:]] or [4, 8]
+    rows_list = [int(a) for a in sys.argv[1:] if int(a) > 0] if len(sys.argv) > 1 else [4, 8]
     tot_m = tot_b = 0.0
     for R in rows_list:
         print(f"=== rows {R}")
