@@ -181,6 +181,17 @@ int sdx_pipeline_report(sdx_pipeline* p, int stream, sdx_report* out);
 /* Per-stream gate decisions of every examined frame so far (in seq order). */
 int sdx_pipeline_decisions(sdx_pipeline* p, int stream, int* out, int cap, int* count);
 int sdx_pipeline_sync(sdx_pipeline* p);
+/* Per-tick trace of stream `stream` (the engine's TickLogEntry log, engine.hpp:43-50,
+ * engine.cpp:181-192): one entry per tick; ingested / emitted are -1 for "none";
+ * calls / element_evals are the tick's denoiser counters; elapsed_ns is the device
+ * time of the iteration when stage profiling is on, else 0.  Entries beyond `cap` are
+ * counted but not copied.  The first 2^20 ticks of a run are kept. */
+typedef struct sdx_trace_entry {
+    int64_t tick, ingested, emitted;
+    uint64_t calls, element_evals;
+    int64_t elapsed_ns;
+} sdx_trace_entry;
+int sdx_pipeline_trace(sdx_pipeline* p, int stream, sdx_trace_entry* out, int cap, int* count);
 /* Error message of an incomplete stream ("" when complete). */
 const char* sdx_pipeline_error_message(sdx_pipeline* p, int stream);
 /* Benchmark path: stage ring_depth iterations of frames (ring_depth x S x

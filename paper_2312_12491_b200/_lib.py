@@ -43,6 +43,11 @@ class sdx_pipeline_config(C.Structure):
                 ("max_skip", C.c_int), ("ring_depth", C.c_int), ("graph", C.c_int)]
 
 
+class sdx_trace_entry(C.Structure):
+    _fields_ = [("tick", C.c_int64), ("ingested", C.c_int64), ("emitted", C.c_int64), ("calls", C.c_uint64),
+                ("element_evals", C.c_uint64), ("elapsed_ns", C.c_int64)]
+
+
 class sdx_report(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "frames_in", "frames_out", "duplicates", "stale_skips", "input_drops", "output_drops", "ticks",
@@ -87,6 +92,7 @@ _sig = {
     "sdx_pipeline_pop": (C.c_int, [P, C.c_int, C.POINTER(C.c_int64), C.c_void_p, C.POINTER(C.c_int)]),
     "sdx_pipeline_report": (C.c_int, [P, C.c_int, C.POINTER(sdx_report)]),
     "sdx_pipeline_decisions": (C.c_int, [P, C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int)]),
+    "sdx_pipeline_trace": (C.c_int, [P, C.c_int, C.POINTER(sdx_trace_entry), C.c_int, C.POINTER(C.c_int)]),
     "sdx_pipeline_sync": (C.c_int, [P]),
     "sdx_pipeline_error_message": (C.c_char_p, [P, C.c_int]),
     "sdx_pipeline_device_time_ms": (C.c_int, [P, C.POINTER(C.c_float)]),

@@ -213,6 +213,16 @@ int sdx_pipeline_decisions(sdx_pipeline* p, int stream, int* out, int cap, int* 
         *count = n;
     });
 }
+int sdx_pipeline_trace(sdx_pipeline* p, int stream, sdx_trace_entry* out, int cap, int* count) {
+    return guarded([&] {
+        NEED(p);
+        NEED(count);
+        const auto& v = p->impl.trace(stream);
+        const int n = static_cast<int>(v.size());
+        if (out && cap > 0) std::memcpy(out, v.data(), sizeof(sdx_trace_entry) * static_cast<size_t>(n < cap ? n : cap));
+        *count = n;
+    });
+}
 int sdx_pipeline_sync(sdx_pipeline* p) {
     return guarded([&] {
         NEED(p);

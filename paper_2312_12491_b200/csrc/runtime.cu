@@ -703,6 +703,12 @@ void Pipeline::process(int k, bool frame_present) {
         kcount_ += 1;
     }
     const size_t cap8 = static_cast<size_t>(e.queue_capacity) * 8;
+    int64_t iter_ns = 0;  // device time of this iteration (stage profiling only)
+    if (profile_) {
+        float ms = 0.f;
+        SDX_CUDA(cudaEventElapsedTime(&ms, kt_[static_cast<size_t>(k) * kMarks], kt_[static_cast<size_t>(k) * kMarks + kMarks - 1]));
+        iter_ns = static_cast<int64_t>(static_cast<double>(ms) * 1e6);
+    }
     for (int s = 0; s < S_; ++s) {
         StreamHost& h = st_[static_cast<size_t>(s)];
         if (h.incomplete) continue;
@@ -719,8 +725,14 @@ void Pipeline::process(int k, bool frame_present) {
             if (skip) h.pending_skips.push_back(L.seq_in);
             else h.eng->ingest(L.seq_in);
         }
+        const bool ingested_now = frame_present && !(e.ssf_enabled && L.decision == SDX_GATE_SKIP);
         if (!h.eng->idle()) {
+            const uint64_t calls0 = h.eng->calls, evals0 = h.eng->evals;
             const auto t = h.eng->tick();
+            if (h.trace.size() < (size_t(1) << 20))
+                h.trace.push_back(sdx_trace_entry{h.eng->ticks(), ingested_now ? static_cast<int64_t>(L.seq_in) : -1,
+                                                  t.emitted ? t.seq : -1, h.eng->calls - calls0, h.eng->evals - evals0,
+                                                  iter_ns});
             if (t.emitted != (L.emit_seq >= 0) || (t.emitted && t.seq != L.emit_seq)) {
                 h.incomplete = true;
                 h.error = "device/host engine mirror diverged";
@@ -876,6 +888,11 @@ bool Pipeline::pop(int stream, int64_t* seq, void* payload) {
     *seq = o.seq;
     if (payload && o.payload) std::memcpy(payload, o.payload->data(), o.payload->size());
     return true;
+}
+
+const Pipeline::StreamHost& Pipeline::host(int stream) const {
+    if (stream < 0 || stream >= S_) raise(SDX_INVALID_ARGUMENT, "pipeline: stream index out of range");
+    return st_[static_cast<size_t>(stream)];
 }
 
 sdx_report Pipeline::report(int stream) const {

@@ -147,7 +147,8 @@ class Pipeline {
     const std::string& error(int stream) const;
     bool pop(int stream, int64_t* seq, void* payload);
     sdx_report report(int stream) const;
-    const std::vector<int>& decisions(int stream) const { return st_[stream].decisions; }
+    const std::vector<int>& decisions(int stream) const { return host(stream).decisions; }
+    const std::vector<sdx_trace_entry>& trace(int stream) const { return host(stream).trace; }
     void sync();
     void reset_timer();
     float device_time_ms();
@@ -167,6 +168,8 @@ class Pipeline {
         int64_t seq;
         std::shared_ptr<std::vector<uint8_t>> payload;
     };
+    struct StreamHost;
+    const StreamHost& host(int stream) const;
     struct StreamHost {
         std::unique_ptr<EngineMirror> eng;
         std::deque<int64_t> pending_skips;
@@ -174,6 +177,7 @@ class Pipeline {
         std::deque<Out> sink;
         std::vector<int64_t> lats;
         std::vector<int> decisions;
+        std::vector<sdx_trace_entry> trace;  // one per tick (TickLogEntry), first 2^20 kept
         uint64_t frames_in = 0, frames_out = 0, duplicates = 0, stale = 0, output_drops = 0;
         uint64_t examined = 0, skipped = 0;
         bool incomplete = false;

@@ -411,6 +411,21 @@ class Pipeline:
                                             C.byref(n)))
         return out
 
+    def trace(self, stream: int = 0) -> list[dict]:
+        """Per-tick log (TickLogEntry, engine.hpp:43-50) of one stream: tick, ingested /
+        emitted sequence ids (None for no frame), denoiser calls / element evals, and the
+        iteration's device time (ns, 0 unless stage profiling is on)."""
+        n = C.c_int()
+        _check(L.lib.sdx_pipeline_trace(self._h, stream, None, 0, C.byref(n)))
+        buf = (L.sdx_trace_entry * max(1, n.value))()
+        _check(L.lib.sdx_pipeline_trace(self._h, stream, buf, n.value, C.byref(n)))
+        out = []
+        for e in buf[:n.value]:
+            out.append({"tick": e.tick, "ingested": None if e.ingested < 0 else e.ingested,
+                        "emitted": None if e.emitted < 0 else e.emitted, "calls": e.calls,
+                        "element_evals": e.element_evals, "elapsed_ns": e.elapsed_ns})
+        return out
+
     def reset_timer(self):
         _check(L.lib.sdx_pipeline_reset_timer(self._h))
 

@@ -5,6 +5,8 @@
 // the reference build).  Run by tests/test_dropin_gpu.py on a B200.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <fstream>
 #include <map>
 #include <random>
 #include <string>
@@ -219,6 +221,89 @@ static void runtime_pipeline() {
     CHECK(r.incomplete && !r.error.empty());
 }
 
+// test_runtime.cpp:145-167 — tick trace: one JSON line per tick; test_runtime.cpp:263-301 —
+// threaded mode (three host threads, bounded queues): strict FIFO delivers every frame in
+// order with no drops; freshest-wins keeps sink ids strictly increasing and never drops at
+// the output
+static void runtime_trace_and_threaded() {
+    {
+        EngineConfig cfg;
+        cfg.n_steps = 2;
+        cfg.d_latent = 256;
+        const auto frames = u8_frames(1, 256, 9, 10);
+        PipelineOptions opts;
+        opts.trace_path = "/tmp/stagger_b200_trace_test.jsonl";
+        const auto rep = run_pipeline(cfg, vector_source(frames), [](const Frame&) {}, opts);
+        CHECK(!rep.incomplete);
+        std::ifstream in(opts.trace_path);
+        CHECK(in.good());
+        std::string line;
+        std::uint64_t lines = 0;
+        std::int64_t last_tick = 0;
+        bool keys = true;
+        while (std::getline(in, line)) {
+            keys = keys && line.find("\"tick\":") != std::string::npos && line.find("\"element_evals\":") != std::string::npos &&
+                   line.find("\"ingested\":") != std::string::npos && line.find("\"emitted\":") != std::string::npos;
+            const std::int64_t t = std::atoll(line.c_str() + 8);
+            keys = keys && t == last_tick + 1;
+            last_tick = t;
+            ++lines;
+        }
+        CHECK(keys);
+        CHECK(lines == rep.ticks && lines > 0);
+        std::remove(opts.trace_path.c_str());
+    }
+    {
+        EngineConfig cfg;
+        cfg.n_steps = 4;
+        cfg.seed = 41;
+        cfg.d_latent = 512;
+        cfg.queue_capacity = 256;  // strict FIFO timing-style run: no drops
+        PipelineOptions opts;
+        opts.threaded = true;
+        opts.strict_fifo = true;
+        std::vector<Frame> got;
+        const auto frames = u8_frames(2, 512, 41, 200);
+        const auto rep = run_pipeline(cfg, vector_source(frames), [&](const Frame& f) { got.push_back(f); }, opts);
+        CHECK(!rep.incomplete);
+        CHECK(rep.mode == "threaded");
+        CHECK(got.size() == 200);
+        CHECK(rep.input_drops == 0);
+        bool inc = true;
+        for (size_t i = 1; i < got.size(); ++i) inc = inc && got[i].seq_id > got[i - 1].seq_id;
+        CHECK(inc);
+        CHECK(rep.wall_ms > 0.0);
+        // same frames deterministically: identical outputs (the device pipeline is the same)
+        std::vector<Frame> ref;
+        run_pipeline(cfg, vector_source(frames), [&](const Frame& f) { ref.push_back(f); });
+        bool same = ref.size() == got.size();
+        for (size_t i = 0; same && i < got.size(); ++i)
+            same = got[i].seq_id == ref[i].seq_id && got[i].payload == ref[i].payload;
+        CHECK(same);
+    }
+    {
+        EngineConfig cfg;
+        cfg.n_steps = 2;
+        cfg.seed = 43;
+        cfg.d_latent = 4096;
+        cfg.queue_capacity = 2;
+        PipelineOptions opts;
+        opts.threaded = true;
+        opts.strict_fifo = false;  // freshest-wins
+        std::vector<Frame> got;
+        const auto frames = u8_frames(2, 4096, 43, 300);
+        const auto rep = run_pipeline(cfg, vector_source(frames), [&](const Frame& f) { got.push_back(f); }, opts);
+        CHECK(!rep.incomplete);
+        CHECK(rep.output_drops == 0);
+        CHECK(rep.frames_in == 300);
+        CHECK(rep.frames_out + rep.input_drops >= 300 - 2 * 4);
+        CHECK(!got.empty());
+        bool inc = true;
+        for (size_t i = 1; i < got.size(); ++i) inc = inc && got[i].seq_id > got[i - 1].seq_id;
+        CHECK(inc);
+    }
+}
+
 // test_ssf.cpp:97-156 — device gate
 static void ssf_gate() {
     SsfState state(0.98, Rng(2));
@@ -249,6 +334,7 @@ int main() {
     stream_batch_oracle_equivalence();
     stream_batch_errors();
     runtime_pipeline();
+    runtime_trace_and_threaded();
     ssf_gate();
     std::printf("%d checks, %d failed\n", g_checks, g_fail);
     return g_fail == 0 ? 0 : 1;

@@ -131,3 +131,33 @@ def test_pipeline_failure_marks_incomplete(sg):
     with pytest.raises(sg.InvalidArgument):
         p.push(np.ones(3, dtype=np.uint8))
     p.close()
+
+
+@pytest.mark.parametrize("n,mode", [(2, "none"), (4, "cfg"), (3, "onetime_negative")])
+def test_pipeline_tick_trace(sg, orc, n, mode):
+    # engine.cpp:181-192 / pipeline.cpp:135-148: one TickLogEntry per tick, ticks 1..T, each
+    # emission the oldest in-flight frame, per-tick denoiser counters summing to the report's
+    D = 512
+    frames = u8_stream("periodic", D, 17, 40)
+    neg = orc.gaussian(orc.derive_seed(3, 5), D) if mode in ("cfg", "onetime_negative") else None
+    cfg = sg.EngineConfig(n_steps=n, guidance_mode=mode, ssf_enabled=True, seed=3, d_latent=D,
+                          negative_condition=neg)
+    p = sg.Pipeline(cfg, n_streams=1, frame_bytes=D)
+    for f in frames:
+        p.push(f[None])
+    p.finish()
+    p.sync()
+    rep = p.report(0)
+    tr = p.trace(0)
+    p.close()
+    assert len(tr) == rep["ticks"] and [e["tick"] for e in tr] == list(range(1, len(tr) + 1))
+    assert sum(e["calls"] for e in tr) == rep["denoiser_calls"]
+    assert sum(e["element_evals"] for e in tr) == rep["element_evals"]
+    ingested = [e["ingested"] for e in tr if e["ingested"] is not None]
+    emitted = [e["emitted"] for e in tr if e["emitted"] is not None]
+    assert ingested == sorted(ingested) and emitted == sorted(emitted)
+    assert emitted == ingested  # every processed frame is emitted once, in order
+    for e in tr:  # emission happens n ticks after ingestion (latency n)
+        if e["emitted"] is not None:
+            t_in = next(x["tick"] for x in tr if x["ingested"] == e["emitted"])
+            assert e["tick"] - t_in == n - 1

@@ -1,7 +1,4 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python tools/gemm_sweep.py 0 > gpurun_out/gemm_sweep.txt 2>&1
-timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_cfg1.json 2> gpurun_out/bench_cfg1.err
-timeout 600 python bench.py --streams 8 --n-steps 1 --guidance self_negative --no-cpu-baseline > gpurun_out/bench_cfg4.json 2> gpurun_out/bench_cfg4.err
-tail -2 gpurun_out/pytest_gpu.log
+timeout 600 python -m pytest tests/test_pipeline_gpu.py -x -q -k trace > gpurun_out/pytest_k.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_k.log
+tail -25 gpurun_out/pytest_k.log
