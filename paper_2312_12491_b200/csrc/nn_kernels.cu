@@ -48,11 +48,10 @@ __device__ __forceinline__ const bf16* gn_src(const GnPlan& p, int img, int px, 
 // reduction), then one 2^-20 fixed-point int64 atomic per (group, moment) into
 // p.acc — integer adds are associative, so the totals are deterministic and no
 // block has to wait for the others.
-__global__ void __launch_bounds__(320) gn_stats_kernel(GnPlan p) {
-    pdl_launch();
-    pdl_wait();
-    const int img = blockIdx.y;
-    if (p.rows_dev && img >= *p.rows_dev) return;
+// Statistics of this block's pixel range: fp32 partial sums (fixed-order smem
+// reduction), then one 2^-20 fixed-point int64 atomic per (group, moment) into
+// p.acc — integer adds are associative, so the totals are deterministic.
+__device__ __forceinline__ void gn_block_stats(const GnPlan& p, int img, float* sm) {
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
     const int PY = blockDim.x / noct;
@@ -91,7 +90,6 @@ __global__ void __launch_bounds__(320) gn_stats_kernel(GnPlan p) {
         }
     }
     // fixed-order reduction: per octet over pixel lanes, then per group over octets
-    extern __shared__ float sm[];  // [PY][noct][4]
     float* mine = sm + (static_cast<long long>(py) * noct + ox) * 4;
     if (py < PY) {
         mine[0] = s0;
@@ -123,24 +121,19 @@ __global__ void __launch_bounds__(320) gn_stats_kernel(GnPlan p) {
     }
 }
 
-__global__ void __launch_bounds__(320) gn_apply_kernel(GnPlan p) {
-    pdl_launch();
-    pdl_wait();
-    const int img = blockIdx.y;
-    if (p.rows_dev && img >= *p.rows_dev) return;
+// y = GN(x) (+ SiLU) over this block's pixel range, (mean, rstd) in fp64 from the sums.
+__device__ __forceinline__ void gn_block_apply(const GnPlan& p, int img, float (*st)[2]) {
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
     const int PY = blockDim.x / noct;
     const int ox = threadIdx.x % noct, py = threadIdx.x / noct;
     const int cg = Ct / p.groups;
-    // per-image group statistics (fp64 from the fixed-point sums), once per block
-    __shared__ float st[64][2];
     for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
         const double inv = 1.0 / 1048576.0;
         const double n = static_cast<double>(cg) * p.HW;
         const unsigned long long* acc = p.acc + (static_cast<long long>(img) * p.groups + g) * 2;
-        const double m = static_cast<double>(static_cast<long long>(acc[0])) * inv / n;
-        double var = static_cast<double>(static_cast<long long>(acc[1])) * inv / n - m * m;
+        const double m = static_cast<double>(static_cast<long long>(__ldcg(acc))) * inv / n;
+        double var = static_cast<double>(static_cast<long long>(__ldcg(acc + 1))) * inv / n - m * m;
         if (var < 0) var = 0;
         st[g][0] = static_cast<float>(m);
         st[g][1] = static_cast<float>(1.0 / sqrt(var + p.eps));
@@ -185,6 +178,60 @@ __global__ void __launch_bounds__(320) gn_apply_kernel(GnPlan p) {
             store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v[k]);
         }
     }
+}
+
+__global__ void __launch_bounds__(320) gn_stats_kernel(GnPlan p) {
+    pdl_launch();
+    pdl_wait();
+    const int img = blockIdx.y;
+    if (p.rows_dev && img >= *p.rows_dev) return;
+    extern __shared__ float sm[];  // [PY][noct][4]
+    gn_block_stats(p, img, sm);
+}
+
+__global__ void __launch_bounds__(320) gn_apply_kernel(GnPlan p) {
+    pdl_launch();
+    pdl_wait();
+    const int img = blockIdx.y;
+    if (p.rows_dev && img >= *p.rows_dev) return;
+    __shared__ float st[64][2];
+    gn_block_apply(p, img, st);
+}
+
+// Statistics and apply in one launch: every block adds its partial sums, then
+// waits on a grid-wide arrival counter (zeroed with the statistics arena before
+// each forward) until all blocks have added theirs.  The plan sizes the grid
+// to be co-resident (occupancy-checked), so the wait cannot deadlock; phase 2
+// re-reads the tensor from L2.
+__global__ void __launch_bounds__(320) gn_fused_kernel(GnPlan p) {
+    pdl_launch();
+    pdl_wait();
+    const int img = blockIdx.y;
+    const bool live = !(p.rows_dev && img >= *p.rows_dev);
+    extern __shared__ float sm[];  // [PY][noct][4]
+    if (live) gn_block_stats(p, img, sm);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(p.counter, 1ull);
+        const unsigned long long target = static_cast<unsigned long long>(gridDim.x) * gridDim.y;
+        if (live) {
+            const long long t0 = clock64();
+            while (true) {
+                unsigned long long v;
+                asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p.counter) : "memory");
+                if (v >= target) break;
+                __nanosleep(64);
+                if (clock64() - t0 > (1LL << 34)) {
+                    printf("sdx groupnorm: grid barrier watchdog (block %d,%d)\n", blockIdx.x, blockIdx.y);
+                    asm volatile("trap;");
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (!live) return;
+    gn_block_apply(p, img, reinterpret_cast<float (*)[2]>(sm));
 }
 
 // ---- LayerNorm (one warp per row) ------------------------------------------------
@@ -398,7 +445,8 @@ unsigned grid_for(long long work, int threads) {
 }  // namespace
 
 GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
-                      const float* beta, int silu_, bf16* out, const int* rows_dev, unsigned long long* acc) {
+                      const float* beta, int silu_, bf16* out, const int* rows_dev, unsigned long long* acc,
+                      unsigned long long* counter) {
     GnPlan p{};
     p.x1 = x1;
     p.x2 = x2;
@@ -428,6 +476,29 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
     if (ppb < 8 * PY) ppb = 8 * PY;
     p.px_per_block = ppb;
     p.chunks = (HW + ppb - 1) / ppb;
+    // single-launch variant: grid must be co-resident -> grow the pixel range per block
+    p.counter = counter;
+    p.fused = 0;
+    if (counter) {
+        // opt in with SDX_GN_SINGLE=1: measured slower at 4 rows (0.66 -> 1.04 ms per forward),
+        // the co-residency limit forces fewer, longer blocks and the barrier wait is exposed
+        static const bool on = [] {
+            const char* v = std::getenv("SDX_GN_SINGLE");
+            return v && v[0] == '1';
+        }();
+        const int threads = noct * PY;
+        const size_t smem = static_cast<size_t>(threads) * 4 * sizeof(float);
+        int per_sm = 0;
+        SDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gn_fused_kernel, threads, smem));
+        const long long cap = static_cast<long long>(per_sm) * 148;
+        if (on && cap > 0) {
+            int fppb = ppb;
+            while (static_cast<long long>((HW + fppb - 1) / fppb) * imgs > cap) fppb += 8 * PY;
+            p.fused = 1;
+            p.px_per_block = fppb;
+            p.chunks = (HW + fppb - 1) / fppb;
+        }
+    }
     return p;
 }
 
@@ -438,6 +509,11 @@ void run_groupnorm(const GnPlan& p, cudaStream_t st) {
     const int noct = Ct / 8;
     const int PY = noct >= 256 ? 1 : 256 / noct;
     const int threads = noct * PY;
+    if (p.fused && !p.stats_fused) {
+        launch_pdl(gn_fused_kernel, dim3(p.chunks, p.imgs), dim3(threads), static_cast<size_t>(threads) * 4 * sizeof(float),
+                   st, p);
+        return;
+    }
     if (!p.stats_fused) {  // statistics not accumulated by the producer: standalone pass
         launch_pdl(gn_stats_kernel, dim3(p.chunks, p.imgs), dim3(threads), static_cast<size_t>(threads) * 4 * sizeof(float), st, p);
     }

@@ -26,11 +26,16 @@ struct GnPlan {
     unsigned long long* acc;
     int stats_fused;
     int px_per_block, chunks;  // pixel range per block (both kernels), blocks per image
+    // single-launch statistics + apply (gn_fused_kernel): grid-wide arrival counter,
+    // zeroed with the arena before each forward; fused = grid fits co-resident
+    unsigned long long* counter;
+    int fused;
     int imgs;
     const int* rows_dev;
 };
 GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
-                      const float* beta, int silu, bf16* out, const int* rows_dev, unsigned long long* acc);
+                      const float* beta, int silu, bf16* out, const int* rows_dev, unsigned long long* acc,
+                      unsigned long long* counter = nullptr);
 void run_groupnorm(const GnPlan& p, cudaStream_t st);
 void free_groupnorm(GnPlan& p);
 

@@ -60,11 +60,11 @@ void UNet::gemm_op(const std::string& kind, const GemmPlan& p) {
 
 GnPlan UNet::groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, float eps, const float* g,
                        const float* b, int silu, bf16* out) {
-    const size_t need = static_cast<size_t>(R_) * 32 * 2;
+    const size_t need = static_cast<size_t>(R_) * 32 * 2 + 1;  // sums + grid-barrier counter
     if (gn_acc_used_ + need > gn_acc_elems_) raise(SDX_LOGIC_ERROR, "UNet: GroupNorm statistics arena exhausted");
     unsigned long long* acc = gn_acc_ + gn_acc_used_;
     gn_acc_used_ += need;
-    GnPlan gp = plan_groupnorm(x1, C1, x2, C2, HW, R_, eps, g, b, silu, out, rows_dev_, acc);
+    GnPlan gp = plan_groupnorm(x1, C1, x2, C2, HW, R_, eps, g, b, silu, out, rows_dev_, acc, acc + need - 1);
     auto p1 = produced_.find(x1);
     auto p2 = x2 ? produced_.find(x2) : produced_.end();
     // only single-pass fast-epilogue producers (split-K reductions would need per-8-column atomics)
@@ -362,7 +362,7 @@ UNet::UNet(const UNetConfig& cfg, cudaStream_t st) : cfg_(cfg) {
     const int init_rows[2] = {R_, R_};
     SDX_CUDA(cudaMemcpy(rows_buf_, init_rows, sizeof(init_rows), cudaMemcpyHostToDevice));
     rows_dev_ = rows_buf_;  // every planned op reads the live row count from rows_buf_[0]
-    gn_acc_elems_ = static_cast<size_t>(96) * R_ * 32 * 2;
+    gn_acc_elems_ = static_cast<size_t>(96) * (R_ * 32 * 2 + 1);
     gn_acc_ = dev_alloc<unsigned long long>(gn_acc_elems_);
     allocs_.push_back(gn_acc_);
     ctx_ = act(static_cast<long long>(cfg.n_prompts) * cfg.ctx_len * cfg.ctx_dim);
