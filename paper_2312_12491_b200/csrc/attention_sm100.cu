@@ -78,11 +78,18 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
 // rescaling), so P = exp2(s - m_used) stays <= 256 and never overflows.
 __global__ void __launch_bounds__(320, 1)
     attn_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, AttnArgs a) {
-    const int qp = blockIdx.x;  // pair of q tiles
-    const int head = blockIdx.y;
-    const int img = blockIdx.z;
+    // Work unit -> (image, head, first q tile, tiles).  Pair units (two 128-query tiles sharing
+    // every K/V block) cover the full waves; a remainder that would leave most SMs idle in a
+    // last wave runs as single-tile units in a second launch (a.single).
+    const int npairs = (a.q_len + 2 * BQ - 1) / (2 * BQ);
+    const int lin = static_cast<int>(blockIdx.x) + a.unit_base;
+    const int plin = a.single ? a.pair_base + lin / 2 : lin;  // linear pair index, q pair fastest
+    const int qp = plin % npairs;
+    const int head = (plin / npairs) % a.heads;
+    const int img = plin / (npairs * a.heads);
+    const int q_first = qp * 2 * BQ + (a.single ? (lin & 1) * BQ : 0);  // first query of this unit
     if (threadIdx.x == 0) pdl_launch();
-    const bool has1 = qp * 2 * BQ + BQ < a.q_len;  // second tile holds live queries
+    const bool has1 = !a.single && q_first + BQ < a.q_len;  // second tile holds live queries
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -102,7 +109,7 @@ __global__ void __launch_bounds__(320, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkv = (a.kv_len + BKV - 1) / BKV;
-    const int q_row0 = img * a.q_rows_per_img + qp * 2 * BQ;
+    const int q_row0 = img * a.q_rows_per_img + q_first;
     const int prompt = a.kv_index ? a.kv_index[img] : img;
     const int kv_row0 = prompt * a.kv_rows_per_img;
 
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(320, 1)
             }
             wait_bar(&pv_done[t], (nkv - 1) & 1);
             tc_fence_after();
-            const int qi = qp * 2 * BQ + t * BQ + r;
+            const int qi = q_first + t * BQ + r;
             float o[HD];
 #pragma unroll
             for (int c = 0; c < HD; c += 16) tmem_ld16(o_addr + c, o + c);
@@ -371,10 +378,26 @@ void run_attention(const AttnPlan& p, cudaStream_t st) {
         SDX_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;
     }
-    dim3 grid((p.a.q_len + 2 * BQ - 1) / (2 * BQ), p.heads, p.images);
     AttnArgs a = p.a;
     a.xmode = g_attn_xmode;
-    launch_pdl(attn_kernel, grid, dim3(320), smem, st, p.tq, p.tkv, a);
+    a.heads = p.heads;
+    const int npairs = (p.a.q_len + 2 * BQ - 1) / (2 * BQ);
+    const int total = npairs * p.heads * p.images;
+    // full waves of pair units; a remainder of R pairs becomes 2R single-tile units when those
+    // fit one wave (a last wave of R << 148 pair CTAs would leave the GPU mostly idle)
+    int full = total;
+    if (total > kSmCount && (total % kSmCount) * 2 <= kSmCount)
+        full = (total / kSmCount) * kSmCount;
+    a.single = 0;
+    a.unit_base = 0;
+    a.pair_base = 0;
+    launch_pdl(attn_kernel, dim3(full), dim3(320), smem, st, p.tq, p.tkv, a);
+    if (full < total) {
+        a.single = 1;
+        a.pair_base = full;
+        const int units = 2 * (total - full);
+        launch_pdl(attn_kernel, dim3(units), dim3(320), smem, st, p.tq, p.tkv, a);
+    }
 }
 
 }  // namespace sdx

@@ -18,6 +18,8 @@ struct AttnArgs {
     const int* rows_dev;          // live image count (device) or null
     float scale;
     int xmode;                    // experiments only: 1 = no MMAs, 2 = no softmax math (pipeline probes)
+    int heads;                    // set by run_attention
+    int single, unit_base, pair_base;  // launch split: pair units, then single-tile units
 };
 
 // Pipeline probe for kernel experiments (results wrong): 0 off, 1 no MMAs, 2 no softmax math.
