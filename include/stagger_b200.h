@@ -64,7 +64,7 @@ typedef struct sdx_config {
     int ssf_enabled;
     double eta;
     uint64_t seed;
-    int cross_frame_attention; /* must be 0 (not built) */
+    int cross_frame_attention; /* Stream Batch attention mix, engine.cpp:139-149 / attention.cpp:12-95 */
     int d_latent;
     int t_grid;
     double entry_strength;

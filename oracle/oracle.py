@@ -50,6 +50,7 @@ class Cfg(C.Structure):
         ("lcm_mode", C.c_int),
         ("codec", C.c_int),
         ("queue_capacity", C.c_int),
+        ("cross_frame_attention", C.c_int),
     ]
 
 
@@ -75,11 +76,12 @@ class Report(C.Structure):
 
 def make_cfg(n_steps=4, guidance_mode="none", gamma=1.4, delta=1.0, ssf_enabled=False,
              eta=0.98, seed=0, d_latent=8, t_grid=1000, entry_strength=1.0,
-             data_variance=1.0, lcm_mode="exact", codec=0, queue_capacity=8) -> Cfg:
+             data_variance=1.0, lcm_mode="exact", codec=0, queue_capacity=8,
+             cross_frame_attention=False) -> Cfg:
     return Cfg(n_steps, GUIDANCE[guidance_mode] if isinstance(guidance_mode, str) else guidance_mode,
                gamma, delta, int(ssf_enabled), eta, seed, d_latent, t_grid, entry_strength,
                data_variance, LCM[lcm_mode] if isinstance(lcm_mode, str) else lcm_mode, codec,
-               queue_capacity)
+               queue_capacity, int(cross_frame_attention))
 
 
 class OracleError(RuntimeError):

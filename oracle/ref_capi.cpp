@@ -81,6 +81,7 @@ struct ref_cfg {
     int lcm_mode;  // 0 exact, 1 boundary_approx
     int codec;     // 0 identity, 1 affine
     int queue_capacity;
+    int cross_frame_attention;
 };
 
 const char* ref_last_error() { return g_err.c_str(); }
@@ -101,6 +102,7 @@ static S::EngineConfig to_cfg(const ref_cfg* c, const double* cond, const double
     cfg.lcm_mode = c->lcm_mode == 1 ? "boundary_approx" : "exact";
     cfg.codec = c->codec == 1 ? "affine" : "identity";
     cfg.queue_capacity = c->queue_capacity;
+    cfg.cross_frame_attention = c->cross_frame_attention != 0;
     if (cond) cfg.condition.assign(cond, cond + c->d_latent);
     if (neg) cfg.negative_condition.assign(neg, neg + c->d_latent);
     return cfg;

@@ -417,6 +417,106 @@ static void consistency(const orc_engine* e, const double* x, int step, int next
     }
 }
 
+/* Cross-frame (Stream Batch) attention, engine.cpp:139-149 with attention.cpp:12-95:
+ * every in-flight frame's guided eps is replaced by attention of its current latent
+ * (lifted to kAttentionTokens = 4 identical token rows of width d) over keys = the
+ * in-flight currents and values = their eps (the batch ordered by step index), then
+ * unlifted by averaging the token rows.  The arithmetic follows the reference loop
+ * for loop (fp64, sequential sums), so the result matches the reference build. */
+static int tick_cross_frame(orc_engine* e, uint64_t rows, int64_t* emitted_seq, double* x0_hat, int64_t* ingest_tick,
+                            int64_t* emit_tick, uint64_t* calls, uint64_t* evals) {
+    const int b = e->count, d = e->d, mode = e->cfg.guidance_mode;
+    enum { kTokens = 4 };
+    double* eps = (double*)malloc(sizeof(double) * (size_t)b * (size_t)d);
+    for (int i = 0; i < b; ++i) {
+        slot_t* f = &e->fl[i];
+        const double a = e->alpha[f->step], be = e->beta[f->step];
+        double* ei = eps + (size_t)i * (size_t)d;
+        analytic(e, f->cur, a, be, e->cond, ei);
+        if (mode == 1) analytic(e, f->cur, a, be, e->neg, e->scratch_neg);
+        combine(e, f->cur, a, be, ei, e->scratch_neg, mode == 3 ? f->x0_ref : f->x0);
+    }
+    /* build_attention_batch: frames ordered by step index (distinct per frame) */
+    int* ord = (int*)malloc(sizeof(int) * (size_t)b);
+    for (int i = 0; i < b; ++i) ord[i] = i;
+    for (int i = 1; i < b; ++i)
+        for (int j = i; j > 0 && e->fl[ord[j]].step < e->fl[ord[j - 1]].step; --j) {
+            const int t = ord[j];
+            ord[j] = ord[j - 1];
+            ord[j - 1] = t;
+        }
+    const int nk = b * kTokens;
+    const double inv_sqrt_d = 1.0 / sqrt((double)d);
+    double* scores = (double*)malloc(sizeof(double) * (size_t)nk);
+    double* out = (double*)malloc(sizeof(double) * (size_t)d);
+    double* mixed = (double*)malloc(sizeof(double) * (size_t)b * (size_t)d);
+    for (int i = 0; i < b; ++i) {
+        const double* q = e->fl[i].cur;  /* every token row of the lifted query is cur_i */
+        memset(out, 0, sizeof(double) * (size_t)d);
+        double max_score = -INFINITY;
+        for (int k = 0; k < nk; ++k) {
+            const double* kr = e->fl[ord[k / kTokens]].cur;
+            double dot = 0.0;
+            for (int c = 0; c < d; ++c) dot += q[c] * kr[c];
+            scores[k] = dot * inv_sqrt_d;
+            max_score = scores[k] > max_score ? scores[k] : max_score;
+        }
+        double denom = 0.0;
+        for (int k = 0; k < nk; ++k) {
+            scores[k] = exp(scores[k] - max_score);
+            denom += scores[k];
+        }
+        for (int k = 0; k < nk; ++k) {
+            const double w = scores[k] / denom;
+            const double* vr = eps + (size_t)ord[k / kTokens] * (size_t)d;
+            for (int c = 0; c < d; ++c) out[c] += w * vr[c];
+        }
+        /* unlift_tokens: the kTokens identical rows summed in order, divided by kTokens */
+        double* mi = mixed + (size_t)i * (size_t)d;
+        for (int c = 0; c < d; ++c) {
+            double sum = 0.0;
+            for (int t = 0; t < kTokens; ++t) sum += out[c];
+            mi[c] = sum / (double)kTokens;
+        }
+    }
+    e->ticks += 1;
+    e->calls += 1;
+    e->evals += rows;
+    *emitted_seq = -1;
+    int emit_index = -1, st = 0;
+    for (int i = 0; i < b && !st; ++i) {
+        slot_t* f = &e->fl[i];
+        const int next = f->step + 1;
+        consistency(e, f->cur, f->step, next, mixed + (size_t)i * (size_t)d, f->cur);
+        f->step = next;
+        if (f->step == e->n) {
+            for (int k = 0; k < d; ++k)
+                if (!isfinite(f->cur[k])) st = fail(3, "tick: non-finite latent at emission");
+            if (st) break;
+            *emitted_seq = f->seq;
+            if (x0_hat) memcpy(x0_hat, f->cur, sizeof(double) * (size_t)d);
+            *ingest_tick = f->ingest_tick;
+            *emit_tick = e->ticks;
+            emit_index = i;
+        }
+    }
+    free(eps);
+    free(ord);
+    free(scores);
+    free(out);
+    free(mixed);
+    if (st) return st;
+    if (emit_index >= 0) {
+        free_slot(&e->fl[emit_index]);
+        for (int i = emit_index; i + 1 < e->count; ++i) e->fl[i] = e->fl[i + 1];
+        memset(&e->fl[e->count - 1], 0, sizeof(slot_t));
+        e->count -= 1;
+    }
+    *calls = 1;
+    *evals = rows;
+    return 0;
+}
+
 /* engine.cpp:78-195 */
 int orc_engine_tick(orc_engine* e, int64_t* emitted_seq, double* x0_hat, int64_t* ingest_tick,
                     int64_t* emit_tick, uint64_t* calls, uint64_t* evals) {
@@ -439,6 +539,7 @@ int orc_engine_tick(orc_engine* e, int64_t* emitted_seq, double* x0_hat, int64_t
             }
         }
     }
+    if (e->cfg.cross_frame_attention) return tick_cross_frame(e, rows, emitted_seq, x0_hat, ingest_tick, emit_tick, calls, evals);
     /* eps rows per frame, then the consistency transition.  The reference
      * computes all eps before any update; per-frame rows are independent so
      * the interleaving does not change any value. */

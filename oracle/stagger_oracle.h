@@ -73,6 +73,7 @@ typedef struct orc_cfg {
     int lcm_mode; /* 0 exact, 1 boundary_approx */
     int codec;    /* 0 identity (only identity is restated) */
     int queue_capacity;
+    int cross_frame_attention; /* engine.cpp:139-149, attention.cpp:12-95 */
 } orc_cfg;
 
 typedef struct orc_engine orc_engine;

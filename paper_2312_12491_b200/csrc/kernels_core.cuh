@@ -30,6 +30,8 @@ struct StepArgs {
     const int* slot_row_n;      // [S][kMaxSteps] negative / init row or -1
     float* emitted;             // [S][d]
     StreamCtl* ctl;
+    float* xfa_eps;             // cross-frame attention: [S][n][d] guided eps, or null (off)
+    double* xfa_dots;           // [S][n][n] latent dot products
 };
 
 struct SsfArgs {

@@ -110,7 +110,7 @@ std::vector<StepScalars> make_step_table(const sdx_step* steps, int n, int lcm_m
 }
 
 void DeviceEngine::init(int S_, int n_, long long d_, int guidance_, double gamma_, double delta_,
-                        const std::vector<StepScalars>& table, bool per_slot_cond_) {
+                        const std::vector<StepScalars>& table, bool per_slot_cond_, bool cross_frame) {
     S = S_;
     n = n_;
     d = d_;
@@ -152,6 +152,10 @@ void DeviceEngine::init(int S_, int n_, long long d_, int guidance_, double gamm
     slot_row_c = dev_alloc<int>(static_cast<size_t>(S) * kMaxSteps);
     slot_row_n = dev_alloc<int>(static_cast<size_t>(S) * kMaxSteps);
     log = dev_alloc<LogEntry>(static_cast<size_t>(S));
+    if (cross_frame) {
+        xfa_eps = dev_alloc<float>(snd);
+        xfa_dots = dev_alloc<double>(static_cast<size_t>(S) * n * n);
+    }
 }
 
 void DeviceEngine::release() {
@@ -159,7 +163,8 @@ void DeviceEngine::release() {
                     static_cast<void*>(x0ref), static_cast<void*>(eps_cached), static_cast<void*>(cond),
                     static_cast<void*>(neg), static_cast<void*>(emitted), static_cast<void*>(ctl),
                     static_cast<void*>(rows), static_cast<void*>(n_rows), static_cast<void*>(slot_row_c),
-                    static_cast<void*>(slot_row_n), static_cast<void*>(log)})
+                    static_cast<void*>(slot_row_n), static_cast<void*>(log), static_cast<void*>(xfa_eps),
+                    static_cast<void*>(xfa_dots)})
         dev_free(p);
     tbl = nullptr;
 }
@@ -186,6 +191,8 @@ StepArgs DeviceEngine::step_args() const {
     a.slot_row_n = slot_row_n;
     a.emitted = emitted;
     a.ctl = ctl;
+    a.xfa_eps = xfa_eps;
+    a.xfa_dots = xfa_dots;
     return a;
 }
 
@@ -232,7 +239,6 @@ Engine::Engine(const sdx_config& cfg, const sdx_step* steps, int n, const double
     : cfg_(cfg), device_(device), mirror_(cfg.n_steps, cfg.guidance_mode) {
     const std::string errs = config_errors(cfg);
     if (!errs.empty()) raise(SDX_INVALID_ARGUMENT, errs);
-    if (cfg.cross_frame_attention) raise(SDX_UNSUPPORTED, "cross_frame_attention is not built (SURVEY §8f)");
     if (cfg.backend != SDX_BACKEND_ANALYTIC)
         raise(SDX_UNSUPPORTED, "engine API: the UNet backend runs through sdx_pipeline");
     if (n != cfg.n_steps) raise(SDX_INVALID_ARGUMENT, "StreamBatchEngine: schedule length != n_steps");
@@ -246,7 +252,8 @@ Engine::Engine(const sdx_config& cfg, const sdx_step* steps, int n, const double
     SDX_CUDA(cudaEventCreate(&ev0_));
     SDX_CUDA(cudaEventCreate(&ev1_));
     const auto table = make_step_table(steps, n, cfg.lcm_mode, cfg.data_variance);
-    dev_.init(1, n, cfg.d_latent, cfg.guidance_mode, cfg.gamma, cfg.delta, table, /*per_slot_cond=*/true);
+    dev_.init(1, n, cfg.d_latent, cfg.guidance_mode, cfg.gamma, cfg.delta, table, /*per_slot_cond=*/true,
+              cfg.cross_frame_attention != 0);
     const size_t d = static_cast<size_t>(cfg.d_latent);
     upload_f32(dev_.eps_cached, eps_cached, static_cast<size_t>(n) * d, stream_);
     if (dev_.neg && neg) upload_f32(dev_.neg, neg, d, stream_);
@@ -431,7 +438,6 @@ Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const 
     const auto& e = cfg.engine;
     const std::string errs = config_errors(e);
     if (!errs.empty()) raise(SDX_INVALID_ARGUMENT, errs);
-    if (e.cross_frame_attention) raise(SDX_UNSUPPORTED, "cross_frame_attention is not built (SURVEY §8f)");
     if (S_ < 1 || S_ > 1024) raise(SDX_INVALID_ARGUMENT, "n_streams must lie in [1,1024]");
     if (e.codec == SDX_CODEC_IDENTITY && D_ != d_)
         raise(SDX_INVALID_ARGUMENT, "LatentCodec::encode: dim mismatch");
@@ -449,7 +455,8 @@ Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const 
     SDX_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     SDX_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
     const auto table = make_step_table(steps, n_, e.lcm_mode, e.data_variance);
-    dev_.init(S_, n_, d_, e.guidance_mode, e.gamma, e.delta, table, /*per_slot_cond=*/false);
+    dev_.init(S_, n_, d_, e.guidance_mode, e.gamma, e.delta, table, /*per_slot_cond=*/false,
+              e.cross_frame_attention != 0);
     const size_t d = static_cast<size_t>(d_);
     upload_f32(dev_.eps_cached, eps_cached, static_cast<size_t>(S_) * n_ * d, stream_);
     upload_f32(dev_.cond, cond, static_cast<size_t>(S_) * d, stream_);

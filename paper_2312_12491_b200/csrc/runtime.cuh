@@ -75,9 +75,11 @@ struct DeviceEngine {
     int* n_rows = nullptr;
     int *slot_row_c = nullptr, *slot_row_n = nullptr;
     LogEntry* log = nullptr;  // [S]
+    float* xfa_eps = nullptr;     // cross-frame attention buffers (null when off)
+    double* xfa_dots = nullptr;
 
     void init(int S_, int n_, long long d_, int guidance_, double gamma_, double delta_,
-              const std::vector<StepScalars>& table, bool per_slot_cond_);
+              const std::vector<StepScalars>& table, bool per_slot_cond_, bool cross_frame = false);
     void release();
     StepArgs step_args() const;
 };

@@ -31,10 +31,11 @@ __device__ __forceinline__ float4 ld4(const float* p) { return __ldcs(reinterpre
 __device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
 __device__ __forceinline__ void st4(float* p, float4 v) { __stcs(reinterpret_cast<float4*>(p), v); }
 
+// guided eps of one element (combine_row, engine.cpp:17-32)
 template <int kMode, bool kExt>
-__device__ __forceinline__ float step1(float x, float mu, float ng, float ref, float ren, float ec_in, float en_in,
-                                       const StepScalars& st, const StepScalars& st0, const StepScalars& nx,
-                                       float gamma, float delta, bool init_now, bool terminal, float* x0ref_out) {
+__device__ __forceinline__ float combine1(float x, float mu, float ng, float ref, float ec_in, float en_in,
+                                          const StepScalars& st, const StepScalars& st0, float gamma, float delta,
+                                          bool init_now, float* x0ref_out) {
     const float ec = kExt ? ec_in : st.f_an * (x - st.f_sa * mu);
     float eps = ec;
     if (kMode == SDX_GUIDANCE_CFG) {
@@ -52,9 +53,23 @@ __device__ __forceinline__ float step1(float x, float mu, float ng, float ref, f
             eps = dv + gamma * (ec - dv);
         }
     }
+    return eps;
+}
+
+// consistency_step + re-noise (schedule.cpp:91-107)
+__device__ __forceinline__ float update1(float x, float eps, float ren, const StepScalars& st, const StepScalars& nx,
+                                         bool terminal) {
     const float px0 = (x - st.f_sb * eps) * st.f_isa;
     const float xh = st.f_cs * x + st.f_co * px0;
     return terminal ? xh : nx.f_sa * xh + nx.f_sb * ren;
+}
+
+template <int kMode, bool kExt>
+__device__ __forceinline__ float step1(float x, float mu, float ng, float ref, float ren, float ec_in, float en_in,
+                                       const StepScalars& st, const StepScalars& st0, const StepScalars& nx,
+                                       float gamma, float delta, bool init_now, bool terminal, float* x0ref_out) {
+    return update1(x, combine1<kMode, kExt>(x, mu, ng, ref, ec_in, en_in, st, st0, gamma, delta, init_now, x0ref_out),
+                   ren, st, nx, terminal);
 }
 
 #define SDX_COMP(c) c
@@ -219,8 +234,145 @@ __global__ void __launch_bounds__(256) step_scalar_kernel(StepArgs a) {
     }
 }
 
+// ---- cross-frame (Stream Batch) attention, engine.cpp:139-149 / attention.cpp:12-95 ----
+// With kAttentionTokens identical token rows per frame (lift_tokens), attention of
+// frame i's latent over the in-flight latents (keys) and guided eps (values)
+// reduces to eps_i <- sum_f softmax_f(x_i . x_f / sqrt(d)) eps_f; unlift_tokens
+// averages identical rows.  Three launches per tick: guided eps (+ entry noising
+// into x_cur), the fp64 dot table, then the mix + consistency step.
+
+// 1. guided eps of every in-flight slot into xfa_eps; the entering frame's x into x_cur
+template <int kMode, bool kExt>
+__global__ void __launch_bounds__(256) xfa_eps_kernel(StepArgs a) {
+    const int s = blockIdx.z, slot = blockIdx.y;
+    const StreamCtl* cp = a.ctl + s;
+    if (!cp->tick_now) return;
+    const SlotCtl sc = cp->slot[slot];
+    if (sc.seq < 0) return;
+    const int step = static_cast<int>(cp->ticks - sc.ingest_tick);
+    const bool entering = sc.entering != 0;
+    const bool init_now = kMode == SDX_GUIDANCE_ONETIME_NEGATIVE && sc.init == 0;
+    const StepScalars st = a.tbl[step];
+    const StepScalars st0 = a.tbl[0];
+    const float g = static_cast<float>(a.gamma), dl = static_cast<float>(a.delta);
+    const long long d = a.d;
+    const long long sd = static_cast<long long>(s) * a.n + slot;
+    const float* x0 = a.x0 + sd * d;
+    float* xcur = a.x_cur + sd * d;
+    float* x0ref = a.x0ref ? a.x0ref + sd * d : nullptr;
+    float* eo = a.xfa_eps + sd * d;
+    const float* e0 = a.eps_cached + (static_cast<long long>(s) * a.n) * d;
+    const float* mu = a.cond + s * a.cond_stream_stride + slot * a.cond_slot_stride;
+    const float* ng = a.neg ? a.neg + static_cast<long long>(s) * d : nullptr;
+    const float* ecr = nullptr;
+    const float* enr = nullptr;
+    if (kExt) {
+        ecr = a.eps_ext + static_cast<long long>(a.slot_row_c[s * kMaxSteps + slot]) * a.eps_ext_stride;
+        const int rn = a.slot_row_n[s * kMaxSteps + slot];
+        enr = rn >= 0 ? a.eps_ext + static_cast<long long>(rn) * a.eps_ext_stride : nullptr;
+    }
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < d;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const float x = entering ? st0.f_sa * x0[i] + st0.f_sb * e0[i] : xcur[i];
+        if (entering) xcur[i] = x;
+        float ref = 0.f;
+        if (kMode == SDX_GUIDANCE_SELF_NEGATIVE) ref = x0[i];
+        if (kMode == SDX_GUIDANCE_ONETIME_NEGATIVE && !init_now) ref = x0ref[i];
+        const float m = kExt ? 0.f : mu[i];
+        const float n_ = (!kExt && ng) ? ng[i] : 0.f;
+        const float ec = kExt ? ecr[i] : 0.f;
+        const float en = (kExt && enr) ? enr[i] : 0.f;
+        float xr = 0.f;
+        eo[i] = combine1<kMode, kExt>(x, m, n_, ref, ec, en, st, st0, g, dl, init_now, &xr);
+        if (kMode == SDX_GUIDANCE_ONETIME_NEGATIVE && init_now) x0ref[i] = xr;
+    }
+}
+
+// 2. dots[s][i][f] = x_i . x_f in fp64 for every in-flight slot pair (one block per pair)
+__global__ void __launch_bounds__(256) xfa_dots_kernel(StepArgs a) {
+    const int s = blockIdx.z, i = blockIdx.y, f = blockIdx.x;
+    const StreamCtl* cp = a.ctl + s;
+    if (!cp->tick_now || cp->slot[i].seq < 0 || cp->slot[f].seq < 0) return;
+    const long long d = a.d;
+    const float* xi = a.x_cur + (static_cast<long long>(s) * a.n + i) * d;
+    const float* xf = a.x_cur + (static_cast<long long>(s) * a.n + f) * d;
+    double acc = 0.0;
+    for (long long k = threadIdx.x; k < d; k += blockDim.x) acc += static_cast<double>(xi[k]) * xf[k];
+    __shared__ double red[256];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off; off >>= 1) {
+        if (static_cast<int>(threadIdx.x) < off) red[threadIdx.x] += red[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.xfa_dots[(static_cast<long long>(s) * a.n + i) * a.n + f] = red[0];
+}
+
+// 3. eps_i <- sum_f w_if eps_f (softmax in fp64 over the in-flight slots), then the
+//    consistency step / emission exactly as the fused step kernel
+template <int kMode>
+__global__ void __launch_bounds__(256) xfa_step_kernel(StepArgs a) {
+    const int s = blockIdx.z, slot = blockIdx.y;
+    const StreamCtl* cp = a.ctl + s;
+    if (!cp->tick_now) return;
+    const SlotCtl sc = cp->slot[slot];
+    if (sc.seq < 0) return;
+    __shared__ float w[kMaxSteps];
+    if (threadIdx.x == 0) {
+        const double* dots = a.xfa_dots + (static_cast<long long>(s) * a.n + slot) * a.n;
+        const double inv_sqrt_d = 1.0 / sqrt(static_cast<double>(a.d));
+        double mx = -INFINITY;
+        for (int f = 0; f < a.n; ++f)
+            if (cp->slot[f].seq >= 0) mx = fmax(mx, dots[f] * inv_sqrt_d);
+        double den = 0.0;
+        for (int f = 0; f < a.n; ++f)
+            if (cp->slot[f].seq >= 0) den += exp(dots[f] * inv_sqrt_d - mx);
+        for (int f = 0; f < a.n; ++f)
+            w[f] = cp->slot[f].seq >= 0 ? static_cast<float>(exp(dots[f] * inv_sqrt_d - mx) / den) : 0.f;
+    }
+    __syncthreads();
+    const int step = static_cast<int>(cp->ticks - sc.ingest_tick);
+    const bool terminal = step + 1 >= a.n;
+    const StepScalars st = a.tbl[step];
+    const StepScalars nx = a.tbl[terminal ? a.n : step + 1];
+    const long long d = a.d;
+    const long long sd = static_cast<long long>(s) * a.n + slot;
+    float* xcur = a.x_cur + sd * d;
+    const float* ren = terminal ? nullptr : a.eps_cached + (static_cast<long long>(s) * a.n + step + 1) * d;
+    float* out = terminal ? a.emitted + static_cast<long long>(s) * d : xcur;
+    const float* eps_s = a.xfa_eps + static_cast<long long>(s) * a.n * d;
+    int bad = 0;
+    for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < d;
+         i += static_cast<long long>(gridDim.x) * blockDim.x) {
+        float e = 0.f;
+        for (int f = 0; f < a.n; ++f)
+            if (w[f] != 0.f) e = fmaf(w[f], eps_s[static_cast<long long>(f) * d + i], e);
+        const float y = update1(xcur[i], e, terminal ? 0.f : ren[i], st, nx, terminal);
+        if (terminal && !isfinite(y)) bad = 1;
+        out[i] = y;
+    }
+    if (terminal) {
+        bad = __syncthreads_or(bad);
+        if (bad && threadIdx.x == 0) atomicOr(&a.ctl[s].nonfinite, 1);
+    }
+}
+
+template <int kMode, bool kExt>
+void launch_xfa(const StepArgs& a, int S, cudaStream_t st) {
+    long long blocks = (a.d + 255) / 256;
+    if (blocks > 1024) blocks = 1024;
+    const dim3 grid(static_cast<unsigned>(blocks), a.n, S);
+    xfa_eps_kernel<kMode, kExt><<<grid, 256, 0, st>>>(a);
+    xfa_dots_kernel<<<dim3(a.n, a.n, S), 256, 0, st>>>(a);
+    xfa_step_kernel<kMode><<<grid, 256, 0, st>>>(a);
+}
+
 template <int kMode, bool kExt>
 void launch_mode(const StepArgs& a, int S, cudaStream_t st) {
+    if (a.xfa_eps) {
+        launch_xfa<kMode, kExt>(a, S, st);
+        return;
+    }
     const int threads = 256;
     const bool vec = (a.d % 4) == 0;
     const long long per_block = threads * (vec ? 8 : 1);

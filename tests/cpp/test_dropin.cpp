@@ -115,6 +115,57 @@ static void stream_batch_oracle_equivalence() {
     }
 }
 
+// test_stream_batch.cpp:284-308 — cross-frame attention changes outputs but not the contract;
+// the drop-in engine (device, fp32) also matches the C restatement with it on
+static void stream_batch_cross_frame() {
+    const int n = 4;
+    auto run = [&](bool mixed, std::map<std::int64_t, Latent>* out, orc_engine** oe) {
+        EngineConfig cfg;
+        cfg.n_steps = n;
+        cfg.cross_frame_attention = mixed;
+        Rng crng(derive_seed(0, kStreamCondition));
+        const Condition cond{"c", sample_gaussian(crng, 8)};
+        StreamBatchEngine engine(cfg, build_precompute(cfg, {cond}), make_backend(cfg));
+        orc_cfg oc = ocfg(cfg);
+        oc.cross_frame_attention = mixed ? 1 : 0;
+        CHECK(orc_engine_create(&oc, cond.embedding.data(), nullptr, oe) == 0);
+        Rng rng(14);
+        std::int64_t seq = 0;
+        double worst = 0.0;
+        auto tick = [&]() {
+            const auto r = engine.tick();
+            std::int64_t es = -1, it = 0, et = 0;
+            std::uint64_t c = 0, ev = 0;
+            Latent ref(8);
+            CHECK(orc_engine_tick(*oe, &es, ref.data(), &it, &et, &c, &ev) == 0);
+            CHECK(bool(r.emitted) == (es >= 0));
+            if (r.emitted) {
+                CHECK(r.emitted->seq_id == es && r.emitted->emit_tick - r.emitted->ingest_tick == n);
+                worst = std::max(worst, max_abs_diff(r.emitted->x0_hat, ref));
+                (*out)[r.emitted->seq_id] = r.emitted->x0_hat;
+            }
+        };
+        for (int f = 0; f < 12; ++f) {
+            const Latent x0 = sample_gaussian(rng, 8);
+            engine.ingest(seq, x0, cond);
+            CHECK(orc_engine_ingest(*oe, seq, x0.data()) == 0);
+            ++seq;
+            tick();
+        }
+        while (!engine.idle()) tick();
+        CHECK(worst <= 1e-3);
+        orc_engine_destroy(*oe);
+    };
+    std::map<std::int64_t, Latent> base, attn;
+    orc_engine* oe = nullptr;
+    run(false, &base, &oe);
+    run(true, &attn, &oe);
+    CHECK(base.size() == attn.size() && base.size() == 12);
+    double diff = 0.0;
+    for (const auto& [seq, v] : base) diff = std::max(diff, max_abs_diff(v, attn.at(seq)));
+    CHECK(diff > 1e-9);  // documented non-equivalence when the mix is on
+}
+
 // test_stream_batch.cpp:62-97 — error contract
 static void stream_batch_errors() {
     EngineConfig cfg;
@@ -332,6 +383,7 @@ static void ssf_gate() {
 
 int main() {
     stream_batch_oracle_equivalence();
+    stream_batch_cross_frame();
     stream_batch_errors();
     runtime_pipeline();
     runtime_trace_and_threaded();

@@ -70,12 +70,6 @@ def test_negative_condition_required(sg):
         sg.StreamBatchEngine(cfg)
 
 
-def test_cross_frame_attention_unsupported(sg):
-    cfg = sg.EngineConfig(n_steps=2, cross_frame_attention=True, d_latent=8)
-    with pytest.raises(sg.Unsupported):
-        sg.StreamBatchEngine(cfg)
-
-
 def test_null_handles_are_rejected():
     from paper_2312_12491_b200 import _lib
 

@@ -17,14 +17,15 @@ MODES = ["none", "cfg", "self_negative", "onetime_negative"]
 TOL = 1e-3
 
 
-def pair(sg, orc, n, mode, d, lcm="exact", seed=0, entry=1.0):
+def pair(sg, orc, n, mode, d, lcm="exact", seed=0, entry=1.0, xfa=False):
     cond = orc.gaussian(orc.derive_seed(seed, 4), d)
     neg = orc.gaussian(orc.derive_seed(seed, 5), d)
     use_neg = neg if mode in ("cfg", "onetime_negative") else None
-    ocfg = make_cfg(n_steps=n, guidance_mode=mode, d_latent=d, lcm_mode=lcm, seed=seed, entry_strength=entry)
+    ocfg = make_cfg(n_steps=n, guidance_mode=mode, d_latent=d, lcm_mode=lcm, seed=seed, entry_strength=entry,
+                    cross_frame_attention=xfa)
     eo = orc.engine(ocfg, cond, use_neg)
     cfg = sg.EngineConfig(n_steps=n, guidance_mode=mode, d_latent=d, lcm_mode=lcm, seed=seed,
-                          entry_strength=entry, negative_condition=use_neg)
+                          entry_strength=entry, negative_condition=use_neg, cross_frame_attention=xfa)
     ed = sg.StreamBatchEngine(cfg)
     return ed, eo, cond
 
@@ -161,3 +162,18 @@ def test_bubbles_advance_partial_batch(sg, orc):
     r = ed.tick()
     assert r.emitted is not None and r.emitted.emit_tick - r.emitted.ingest_tick == n
     assert ed.idle()
+
+
+@pytest.mark.parametrize("mode", MODES)
+@pytest.mark.parametrize("n", [1, 2, 4, 8])
+@pytest.mark.parametrize("d,scale", [(8, 1.0), (64, 0.3), (16384, 0.02)])
+def test_engine_cross_frame_attention_matches_oracle(sg, orc, n, mode, d, scale):
+    # engine.cpp:139-149 + attention.cpp:12-95 on the device (three launches per tick) vs the C
+    # restatement (bit-exact with the reference build): emissions within the fp32 bound, all
+    # tick / ordering observables identical; `scale` keeps the attention weights mixed
+    ed, eo, cond = pair(sg, orc, n, mode, d, xfa=True)
+    rng = np.random.default_rng(29 + n)
+    xs = [scale * rng.standard_normal(d) for _ in range(3 * n + 8)]
+    worst, emitted = drive(ed, eo, cond, xs, bubble_every=5)
+    assert emitted > 0 and worst <= TOL, worst
+    ed.close()

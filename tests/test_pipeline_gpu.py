@@ -34,13 +34,14 @@ def u8_stream(kind, D, seed, n):
     return np.stack(out)
 
 
-def compare(sg, orc, frames, n, mode="none", ssf=True, seed=3, max_skip=0, lcm="exact"):
+def compare(sg, orc, frames, n, mode="none", ssf=True, seed=3, max_skip=0, lcm="exact", xfa=False):
     D = frames.shape[1]
     neg = orc.gaussian(orc.derive_seed(seed, 5), D) if mode in ("cfg", "onetime_negative") else None
-    ocfg = make_cfg(n_steps=n, guidance_mode=mode, ssf_enabled=ssf, seed=seed, d_latent=D, lcm_mode=lcm)
+    ocfg = make_cfg(n_steps=n, guidance_mode=mode, ssf_enabled=ssf, seed=seed, d_latent=D, lcm_mode=lcm,
+                    cross_frame_attention=xfa)
     want = orc.run_pipeline(ocfg, frames.astype(np.float64), neg=neg, max_skip=max_skip)
     cfg = sg.EngineConfig(n_steps=n, guidance_mode=mode, ssf_enabled=ssf, seed=seed, d_latent=D,
-                          negative_condition=neg, lcm_mode=lcm)
+                          negative_condition=neg, lcm_mode=lcm, cross_frame_attention=xfa)
     sink, rep = sg.run_pipeline(cfg, frames, max_skip=max_skip)
     assert [s for s, _ in sink] == want.seq.tolist()
     worst = max((float(np.max(np.abs(p.astype(np.float64) - w))) for (_, p), w in zip(sink, want.payload)),
@@ -161,3 +162,13 @@ def test_pipeline_tick_trace(sg, orc, n, mode):
         if e["emitted"] is not None:
             t_in = next(x["tick"] for x in tr if x["ingested"] == e["emitted"])
             assert e["tick"] - t_in == n - 1
+
+
+@pytest.mark.parametrize("mode", ["none", "self_negative", "onetime_negative"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_pipeline_cross_frame_attention(sg, orc, mode, n):
+    # test_stream_batch.cpp:284-308 (cross-frame attention keeps latency n and ordering) and the
+    # device pipeline's sink / report / payloads against the oracle's run_pipeline with it on
+    frames = u8_stream("periodic", 256, 51 + n, 40)
+    want, sink, rep = compare(sg, orc, frames, n, mode=mode, xfa=True)
+    assert rep["latency_ticks_min"] == rep["latency_ticks_max"] == n

@@ -66,11 +66,7 @@ def conv(imgs, H, cin, cout, stride=1):
                                              out.data_ptr(), 0, 0, 0, hp))
 
 
-conv(1, 64, 64, 64)
-conv(1, 512, 64, 64)
-gemm(256, 1280, 1280)
-gemm(16384, 320, 320)
-gemm(16384, 320, 320, True)
-gemm(1024, 1280, 1280, True)
 conv(4, 64, 320, 320)
+conv(4, 32, 640, 640)
+gemm(16384, 320, 1280, True)
 gemm(8192, 8192, 8192)
