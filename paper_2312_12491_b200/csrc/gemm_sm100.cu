@@ -384,9 +384,8 @@ __global__ void __launch_bounds__(320, 1)
             const int n0 = (t % n_tiles) * BN;
             const int row0 = m0 + q * 32;
             const int row = row0 + lane;
-            wait_bounded(&tfull[acc], (lt >> 1) & 1);
-            if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[4] = gtimer();
-            tc_fence_after();
+            // per-row operands that do not depend on the accumulator are fetched before
+            // waiting for it, so their latency hides under this tile's MMAs
             const float* bimg = nullptr;
             if (e_bimg && row < m_eff) {
                 const long long im = static_cast<long long>(row) / e_rpi;
@@ -408,6 +407,9 @@ __global__ void __launch_bounds__(320, 1)
                 const float var = fmaxf(s2 * inv_c - ln_mean * ln_mean, 0.f);
                 ln_rstd = rsqrtf(var + g.epi.ln_eps);
             }
+            wait_bounded(&tfull[acc], (lt >> 1) & 1);
+            if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[4] = gtimer();
+            tc_fence_after();
             float rs_sum = 0.f, rs_sq = 0.f;  // row statistics of this tile's stored values
             const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
