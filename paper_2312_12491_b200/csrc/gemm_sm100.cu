@@ -124,8 +124,18 @@ __device__ __forceinline__ void gn_sink_chunk(const GemmEpilogue& e, int ngn, co
 // each CTA stages its own 128 A rows and half of the BN B rows, the leader
 // issues the MMAs, every CTA's TMEM holds its 128 output rows x BN and runs its
 // own epilogue.  Halves the per-SM B traffic (L2 and smem) of a 256 x BN tile.
+// Epilogue warps: 12 (3 per TMEM lane quadrant, 2 KB smem box each) on the fast path,
+// whose small-K GEMMs are epilogue-bound; 8 (4 KB fp32 slabs) on the general path.
+template <bool FAST>
+struct EpiCfg {
+    static_assert(kRowStatParts * 4 == 12, "row-statistics partials = fast-path epilogue warps per quadrant");
+    static constexpr int kWarps = FAST ? 12 : 8;
+    static constexpr int kSlab = FAST ? 2048 : 4096;
+    static constexpr int kThreads = 64 + 32 * kWarps;
+};
+
 template <int BN, int STAGES, int AMODE, bool FAST, bool PAIR>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
                    const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap to, const GemmArgs g) {
     static_assert(!PAIR || FAST, "CTA-pair GEMM uses the fast epilogue");
@@ -144,8 +154,9 @@ __global__ void __launch_bounds__(320, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint8_t* slabs = sB + (HALO ? 9 : STAGES) * B_BYTES;  // 8 epilogue warps x 4 KB (1024-aligned)
-    uint64_t* full = reinterpret_cast<uint64_t*>(slabs + 8 * 4096);
+    constexpr int NEPI = EpiCfg<FAST>::kWarps, SLAB = EpiCfg<FAST>::kSlab;
+    uint8_t* slabs = sB + (HALO ? 9 : STAGES) * B_BYTES;  // NEPI epilogue warps x SLAB (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(slabs + NEPI * SLAB);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;   // [2]
     uint64_t* tempty = tfull + 2;       // [2]
@@ -170,7 +181,7 @@ __global__ void __launch_bounds__(320, 1)
         mbar_init(bfull, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull[i], 1);
-            mbar_init(&tempty[i], PAIR ? 16 : 8);  // one arrival per epilogue warp (of both CTAs)
+            mbar_init(&tempty[i], (PAIR ? 2 : 1) * NEPI);  // one arrival per epilogue warp (of both CTAs)
         }
         fence_barrier_init();
     }
@@ -355,7 +366,8 @@ __global__ void __launch_bounds__(320, 1)
         // store per warp (OOB rows / columns clipped by the tensor map).  The
         // residual row segment is fetched before the TMEM load.
         const int q = warp & 3;
-        const int half = (warp - 2) >> 2;
+        const int part = (warp - 2) >> 2;  // which of the quadrant's NEPI/4 warps
+        constexpr int CSTEP = 32 * (NEPI / 4);
         const bool raw = splits > 1;
         const float e_scale = raw ? 1.f : g.epi.scale;
         const float* e_bias = raw ? nullptr : g.epi.bias;
@@ -372,9 +384,8 @@ __global__ void __launch_bounds__(320, 1)
         const float2* e_lnp = raw ? nullptr : g.epi.ln_part;
         const float* e_lns = g.epi.ln_s;
         float2* e_rso = raw ? nullptr : g.epi.row_stats_out;
-        uint8_t* slab = slabs + (warp - 2) * 4096;
+        uint8_t* slab = slabs + (warp - 2) * SLAB;
         const uint32_t slab_s = smem_u32(slab);
-        uint32_t nstore = 0;  // bf16 boxes issued by this warp (double-buffered 2 KB halves)
         uint32_t lt = 0;
         for (int u = ustart; u < total; u += ustep, ++lt) {
             const int t = u / splits;
@@ -413,7 +424,8 @@ __global__ void __launch_bounds__(320, 1)
             float rs_sum = 0.f, rs_sq = 0.f;  // row statistics of this tile's stored values
             const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-            for (int c = half * 32; c < BN; c += 64) {
+            int kc = 0;
+            for (int c = part * 32; c < BN; c += CSTEP, ++kc) {
                 const int col0 = n0 + c;
                 if (col0 >= g.N) break;  // warp-uniform; N % 32 == 0 on this path
                 uint4 rq[4];
@@ -426,7 +438,7 @@ __global__ void __launch_bounds__(320, 1)
                 tmem_ld32_nowait(tbase + c, r);
                 tmem_wait_ld32(r);
                 const bool dstamp = dbg && lt == 0 && warp == 2 && lane == 0;
-                if (dstamp) dbg[7 + 3 * (c / 64)] = gtimer();
+                if (dstamp && kc < 3) dbg[7 + 3 * kc] = gtimer();
                 float v[32];
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]) * e_scale;
@@ -485,38 +497,35 @@ __global__ void __launch_bounds__(320, 1)
                 }
                 const int sw = (lane >> 1) & 3;  // 64-byte swizzle: 16 B chunk j of row r at r*64 + ((j ^ (r>>1 & 3)) * 16)
                 if (raw) {
-                    // fp32 partials: two 16-column boxes (both 2 KB halves of the slab)
-                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    __syncwarp();
+                    // fp32 partials: two 16-column boxes through the warp's 2 KB buffer
 #pragma unroll
                     for (int hb = 0; hb < 2; ++hb) {
-                        uint8_t* rowp = slab + hb * 2048 + lane * 64;
+                        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        __syncwarp();
+                        uint8_t* rowp = slab + lane * 64;
 #pragma unroll
                         for (int j = 0; j < 4; ++j)
                             *reinterpret_cast<float4*>(rowp + ((j ^ sw) << 4)) =
                                 make_float4(v[16 * hb + 4 * j], v[16 * hb + 4 * j + 1], v[16 * hb + 4 * j + 2], v[16 * hb + 4 * j + 3]);
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    __syncwarp();
-                    if (lane == 0) {
-#pragma unroll
-                        for (int hb = 0; hb < 2; ++hb)
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0) {
                             asm volatile(
                                 "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
                                     reinterpret_cast<uint64_t>(&to)),
-                                "r"(col0 + 16 * hb), "r"(row0), "r"(sp), "r"(slab_s + hb * 2048)
+                                "r"(col0 + 16 * hb), "r"(row0), "r"(sp), "r"(slab_s)
                                 : "memory");
-                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                        }
                     }
                 } else if (e_geglu) {
                     // interleaved [16 value | 16 gate] columns -> 16 outputs; 32-byte rows, 32B swizzle
 #pragma unroll
                     for (int i = 0; i < 16; ++i)
                         v[i] = v[i] * 0.5f * v[16 + i] * (1.f + erff(v[16 + i] * 0.70710678118654752f));
-                    const uint32_t buf = nstore & 1;
-                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     __syncwarp();
-                    uint8_t* rowp = slab + buf * 2048 + lane * 32;
+                    uint8_t* rowp = slab + lane * 32;
                     const int sw2 = (lane >> 2) & 1;
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
@@ -532,16 +541,14 @@ __global__ void __launch_bounds__(320, 1)
                     if (lane == 0) {
                         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                          reinterpret_cast<uint64_t>(&to)),
-                                     "r"(col0 / 2), "r"(row0), "r"(slab_s + buf * 2048)
+                                     "r"(col0 / 2), "r"(row0), "r"(slab_s)
                                      : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
-                    ++nstore;
                 } else {
-                    const uint32_t buf = nstore & 1;
-                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     __syncwarp();
-                    uint8_t* rowp = slab + buf * 2048 + lane * 64;
+                    uint8_t* rowp = slab + lane * 64;
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         uint4 o;
@@ -556,16 +563,15 @@ __global__ void __launch_bounds__(320, 1)
                     if (lane == 0) {
                         asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                                          reinterpret_cast<uint64_t>(&to)),
-                                     "r"(col0), "r"(row0), "r"(slab_s + buf * 2048)
+                                     "r"(col0), "r"(row0), "r"(slab_s)
                                      : "memory");
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
-                    ++nstore;
                 }
-                if (dstamp) dbg[9 + 3 * (c / 64)] = gtimer();
+                if (dstamp && kc < 3) dbg[9 + 3 * kc] = gtimer();
             }
             if (e_rso && row < m_eff)
-                e_rso[static_cast<long long>(2 * (t % n_tiles) + half) * g.M + row] = make_float2(rs_sum, rs_sq);
+                e_rso[static_cast<long long>(kRowStatParts * (t % n_tiles) + part) * g.M + row] = make_float2(rs_sum, rs_sq);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {
@@ -999,27 +1005,29 @@ void encode_2d(CUtensorMap* m, const void* ptr, long long rows, long long cols, 
 
 // smem: 1 KB alignment pad + STAGES x (A 16 KB + B BNL x 128 B) + 8 epilogue slabs of
 // 4 KB + barriers; as many stages (<= 8) as fit in 227 KB.
-template <int BN, bool PAIR, int AMODE>
+template <int BN, bool PAIR, int AMODE, bool FAST>
 constexpr int stages_for() {
     if (AMODE == kAHalo) return 2;  // 2 x 49 KB halo boxes next to 72 KB of resident weights
     constexpr int bnl = PAIR ? BN / 2 : BN;
-    constexpr int st = (232448 - 1024 - 8 * 4096 - 256) / (128 * 64 * 2 + bnl * 64 * 2);
+    constexpr int slabs = EpiCfg<FAST>::kWarps * EpiCfg<FAST>::kSlab;
+    constexpr int st = (232448 - 1024 - slabs - 256) / (128 * 64 * 2 + bnl * 64 * 2);
     return st > 8 ? 8 : st;
 }
 
-template <int BN, bool PAIR, int AMODE>
+template <int BN, bool PAIR, int AMODE, bool FAST>
 size_t smem_for() {
-    if (AMODE == kAHalo) return 1024 + 2 * 50176 + 9 * BN * 64 * 2 + 8 * 4096 + 256;
+    constexpr int slabs = EpiCfg<FAST>::kWarps * EpiCfg<FAST>::kSlab;
+    if (AMODE == kAHalo) return 1024 + 2 * 50176 + 9 * BN * 64 * 2 + slabs + 256;
     constexpr int bnl = PAIR ? BN / 2 : BN;
-    return 1024 + static_cast<size_t>(stages_for<BN, PAIR, AMODE>()) * (128 * 64 * 2 + bnl * 64 * 2) + 8 * 4096 + 256;
+    return 1024 + static_cast<size_t>(stages_for<BN, PAIR, AMODE, FAST>()) * (128 * 64 * 2 + bnl * 64 * 2) + slabs + 256;
 }
 
 template <int BN, int AMODE, bool FAST, bool PAIR>
 void launch_t(const GemmPlan& p, cudaStream_t st) {
-    constexpr int S = stages_for<BN, PAIR, AMODE>();
+    constexpr int S = stages_for<BN, PAIR, AMODE, FAST>();
     auto k = gemm_tc_kernel<BN, S, AMODE, FAST, PAIR>;
     static bool attr = false;
-    const size_t smem = smem_for<BN, PAIR, AMODE>();
+    const size_t smem = smem_for<BN, PAIR, AMODE, FAST>();
     if (!attr) {
         SDX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;
@@ -1048,7 +1056,7 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
         const int np = pairs < kSmCount / 2 ? pairs : kSmCount / 2;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * np);
-        cfg.blockDim = dim3(320);
+        cfg.blockDim = dim3(EpiCfg<FAST>::kThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute at[2];
@@ -1064,7 +1072,7 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
     } else {
         const int units = n_tiles * ((p.M + 127) / 128) * p.splits;
         dim3 grid(units < kSmCount ? units : kSmCount);
-        launch_pdl(k, grid, dim3(320), smem, st, p.ta, p.ta2, p.tb, p.to, g);
+        launch_pdl(k, grid, dim3(EpiCfg<FAST>::kThreads), smem, st, p.ta, p.ta2, p.tb, p.to, g);
     }
     if (p.splits > 1) {
         const long long work = static_cast<long long>(p.M) * ((p.N + 7) / 8);

@@ -65,9 +65,11 @@ struct GemmEpilogue {
     float ln_eps = 1e-5f;
     const float* ln_s = nullptr;
     // Row statistics of this GEMM's (bf16-rounded) output for a LayerNorm-folded
-    // consumer: [2 * n_tiles][M] float2, one entry per (N tile, epilogue half) per row.
+    // consumer: [kRowStatParts * n_tiles][M] float2, one entry per (N tile, epilogue
+    // warp of the row's quadrant) per row.
     float2* row_stats_out = nullptr;
 };
+constexpr int kRowStatParts = 3;  // fast-path epilogue warps per TMEM lane quadrant
 
 // A prebuilt launch (tensor maps encoded once; replayable / graph-capturable).
 struct GemmPlan {

@@ -205,7 +205,7 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
         if (fold_on && pp && pp->fast && pp->splits == 1 && !pp->epi.geglu && !pp->epi.row_stats_out &&
             pp->M == static_cast<int>(M) && pp->N == C) {
             const int nt = (pp->N + pp->bn - 1) / pp->bn;
-            float2* rs = dev_alloc<float2>(static_cast<size_t>(2 * nt) * M);
+            float2* rs = dev_alloc<float2>(static_cast<size_t>(kRowStatParts * nt) * M);
             allocs_.push_back(rs);
             pp->epi.row_stats_out = rs;
             bf16* wf = act(static_cast<long long>(N) * C);
@@ -213,7 +213,7 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
             float* cv = actf(N);
             run_ln_fold(w, N, C, lg, lb, bias, wf, sv, cv, nullptr);
             e.ln_part = rs;
-            e.ln_nparts = 2 * nt;
+            e.ln_nparts = kRowStatParts * nt;
             e.ln_C = C;
             e.ln_eps = 1e-5f;
             e.ln_s = sv;
