@@ -122,12 +122,26 @@ __device__ __forceinline__ void gn_block_stats(const GnPlan& p, int img, float* 
 }
 
 // y = GN(x) (+ SiLU) over this block's pixel range, (mean, rstd) in fp64 from the sums.
+// The first batch of pixels is requested before the group statistics are derived,
+// so the load latency overlaps the fp64 math and the barrier.
 __device__ __forceinline__ void gn_block_apply(const GnPlan& p, int img, float (*st)[2]) {
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
     const int PY = blockDim.x / noct;
     const int ox = threadIdx.x % noct, py = threadIdx.x / noct;
     const int cg = Ct / p.groups;
+    const int c = ox * 8;
+    const int px0 = blockIdx.x * p.px_per_block;
+    const int px1 = min(p.HW, px0 + p.px_per_block);
+    float v[8][8];
+    int base = px0 + py;
+    if (py < PY) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int px = base + k * PY;
+            if (px < px1) load8(gn_src(p, img, px, c), v[k]);
+        }
+    }
     for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
         const double inv = 1.0 / 1048576.0;
         const double n = static_cast<double>(cg) * p.HW;
@@ -140,7 +154,6 @@ __device__ __forceinline__ void gn_block_apply(const GnPlan& p, int img, float (
     }
     __syncthreads();
     if (py >= PY) return;
-    const int c = ox * 8;
     const int g0 = c / cg, split = (g0 + 1) * cg - c;
     const float m0 = st[g0][0], r0 = st[g0][1];
     const float m1 = split < 8 ? st[g0 + 1][0] : 0.f, r1 = split < 8 ? st[g0 + 1][1] : 0.f;
@@ -157,15 +170,7 @@ __device__ __forceinline__ void gn_block_apply(const GnPlan& p, int img, float (
             sh[i] = bet[i] - m * r * gam[i];
         }
     }
-    const int px0 = blockIdx.x * p.px_per_block;
-    const int px1 = min(p.HW, px0 + p.px_per_block);
-    for (int base = px0 + py; base < px1; base += 8 * PY) {
-        float v[8][8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int px = base + k * PY;
-            if (px < px1) load8(gn_src(p, img, px, c), v[k]);
-        }
+    while (true) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int px = base + k * PY;
@@ -176,6 +181,13 @@ __device__ __forceinline__ void gn_block_apply(const GnPlan& p, int img, float (
                 v[k][i] = p.silu ? __fdividef(y, 1.f + __expf(-y)) : y;
             }
             store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v[k]);
+        }
+        base += 8 * PY;
+        if (base >= px1) break;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int px = base + k * PY;
+            if (px < px1) load8(gn_src(p, img, px, c), v[k]);
         }
     }
 }
