@@ -52,6 +52,19 @@ __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
     }
 }
 
+// non-blocking probe of an mbarrier phase
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return done != 0;
+}
+
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -163,7 +176,7 @@ __global__ void __launch_bounds__(320, 1)
                 const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ + t * TILE_BYTES));
                 const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + (j % KVS) * TILE_BYTES));
 #pragma unroll
-                for (int k = 0; k < (a.xmode == 1 ? 0 : HD / 16); ++k)
+                for (int k = 0; k < ((a.xmode == 1 || a.xmode == 6 || a.xmode == 7) ? 0 : HD / 16); ++k)
                     umma_f16(tmem + t * 192, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
                 umma_commit(&s_full[t]);
             };
@@ -171,7 +184,7 @@ __global__ void __launch_bounds__(320, 1)
                 const uint32_t pbase = smem_u32(sP + t * 2 * TILE_BYTES);
                 const uint32_t vbase = smem_u32(sV + (j % KVS) * TILE_BYTES);
 #pragma unroll
-                for (int k = 0; k < (a.xmode == 1 ? 0 : BKV / 16); ++k) {
+                for (int k = 0; k < ((a.xmode == 1 || a.xmode == 5 || a.xmode == 7) ? 0 : BKV / 16); ++k) {
                     const uint64_t dp = desc_kmajor_sw128(pbase + (k >> 2) * TILE_BYTES) + 2 * (k & 3);
                     const uint64_t dv = desc_mnmajor_sw128(vbase + k * 2048, 0);
                     umma_f16(tmem + t * 192 + 128, dp, dv, idesc_o, (j > 0 || k != 0) ? 1u : 0u);
@@ -181,22 +194,38 @@ __global__ void __launch_bounds__(320, 1)
             wait_bar(&kv_full[0], 0);
             tc_fence_after();
             for (int t = 0; t < ntile; ++t) issue_s(t, 0);
-            // S_t(j+1) is issued as soon as tile t's softmax has read S_t(j) out of TMEM
-            // (s_free), overlapping that softmax's exponentials; PV_t(j) once P_t(j) is in smem.
-            for (int j = 0; j < nkv; ++j) {
-                const bool more = j + 1 < nkv;
-                if (more) wait_bar(&kv_full[(j + 1) % KVS], ((j + 1) / KVS) & 1);
-                for (int t = 0; t < ntile; ++t) {
-                    if (more) {
-                        wait_bar(&s_free[t], j & 1);
+            // Event-driven issue: per tile, S_t(j) goes out once K_j has landed and the softmax
+            // has read S_t(j-1) out of TMEM (s_free), PV_t(j) once P_t(j) is in smem (p_full).
+            // The barriers are polled without blocking, so one tile's softmax never stalls
+            // the other tile's MMAs; K/V slot j is released after both tiles' PV(j).
+            int ns[2] = {1, ntile > 1 ? 1 : nkv};   // next S block per tile
+            int np[2] = {0, ntile > 1 ? 0 : nkv};   // next PV block per tile
+            int released = 0;                        // K/V blocks released so far
+            const long long t0 = clock64();
+            while (released < nkv) {
+                bool progress = false;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (ns[t] < nkv && ns[t] - np[t] <= 1 && mbar_test(&kv_full[ns[t] % KVS], (ns[t] / KVS) & 1) &&
+                        mbar_test(&s_free[t], (ns[t] - 1) & 1)) {
                         tc_fence_after();
-                        issue_s(t, j + 1);
+                        issue_s(t, ns[t]);
+                        ++ns[t];
+                        progress = true;
                     }
-                    wait_bar(&p_full[t], j & 1);  // P_t(j) in smem, O_t rescaled
-                    tc_fence_after();
-                    issue_pv(t, j);
+                    if (np[t] < ns[t] && mbar_test(&p_full[t], np[t] & 1)) {
+                        tc_fence_after();
+                        issue_pv(t, np[t]);
+                        ++np[t];
+                        progress = true;
+                    }
                 }
-                umma_commit(&kv_empty[j % KVS]);
+                const int done = np[0] < np[1] ? np[0] : np[1];
+                while (released < done) umma_commit(&kv_empty[released++ % KVS]);
+                if (!progress && clock64() - t0 > (1LL << 34)) {
+                    printf("sdx attention: MMA issue watchdog (block %d)\n", blockIdx.x);
+                    asm volatile("trap;");
+                }
             }
         }
         __syncwarp();
@@ -215,11 +244,16 @@ __global__ void __launch_bounds__(320, 1)
                 wait_bar(&s_full[t], j & 1);
                 tc_fence_after();
                 uint32_t sr[128];
-                tmem_ld32_nowait(s_addr + 0, sr);
-                tmem_ld32_nowait(s_addr + 32, sr + 32);
-                tmem_ld32_nowait(s_addr + 64, sr + 64);
-                tmem_ld32_nowait(s_addr + 96, sr + 96);
-                tmem_wait_ld();
+                if (a.xmode == 7) {  // probe: synchronisation skeleton only (no S read)
+#pragma unroll
+                    for (int i = 0; i < 128; ++i) sr[i] = 0u;
+                } else {
+                    tmem_ld32_nowait(s_addr + 0, sr);
+                    tmem_ld32_nowait(s_addr + 32, sr + 32);
+                    tmem_ld32_nowait(s_addr + 64, sr + 64);
+                    tmem_ld32_nowait(s_addr + 96, sr + 96);
+                    tmem_wait_ld();
+                }
                 // S is in registers: the next QK^T may overwrite the TMEM S buffer
                 tc_fence_before();
                 __syncwarp();
@@ -265,7 +299,7 @@ __global__ void __launch_bounds__(320, 1)
                 float sum8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 const float nm = -m_used;
 #pragma unroll
-                for (int c = 0; c < (a.xmode == 2 ? 0 : BKV); c += 16) {
+                for (int c = 0; c < ((a.xmode == 2 || a.xmode == 7) ? 0 : BKV); c += 16) {
                     uint32_t pk[8];
 #pragma unroll
                     for (int i = 0; i < 16; i += 2) {

@@ -42,9 +42,9 @@ for imgs, T, heads in ((4, 4096, 5), (8, 4096, 5), (4, 1024, 10)):
     fn = lambda s: L.sdx_kernel_attention(qkv.data_ptr(), imgs * T, 3 * Cd, 0, qkv.data_ptr(), imgs * T, 3 * Cd, Cd,  # noqa
                                           2 * Cd, out.data_ptr(), Cd, imgs, heads, T, T, T, None, 0.125, s)
     res = []
-    for mode in (0, 1, 2):
+    for mode in (0, 1, 2, 5, 6, 7):
         L.sdx_kernel_attention_probe(mode)
         res.append(timed(fn))
     L.sdx_kernel_attention_probe(0)
     fl = 4.0 * imgs * heads * T * T * 64
-    print(f"attn imgs={imgs} T={T} heads={heads}: full {res[0]:7.1f} us ({fl / res[0] / 1e6:6.1f} TF/s) | no-mma {res[1]:7.1f} | no-softmax {res[2]:7.1f}", flush=True)
+    print(f"attn imgs={imgs} T={T} heads={heads}: full {res[0]:7.1f} us ({fl / res[0] / 1e6:6.1f} TF/s) | no-mma {res[1]:7.1f} | no-softmax {res[2]:7.1f} | no-PV {res[3]:7.1f} | no-S {res[4]:7.1f} | skeleton {res[5]:7.1f}", flush=True)
