@@ -80,6 +80,18 @@ int sdx_unet_profile(sdx_unet* u, int rows, int cap, const char** kinds, float* 
 int sdx_unet_profile_detail(sdx_unet* u, int rows, int cap, const char** labels, double* flops, float* ms,
                             int* count);
 int sdx_memcpy_d2d(void* dst, const void* src, int64_t bytes);
+
+/* The TAESD-class tiny VAE of the pipeline's codec slot on its own (random-init,
+ * seeded): encode n <= imax u8 NHWC 512x512x3 frames (device) to fp32 NHWC 64x64x4
+ * latents (device), decode the reverse (u8 = round(255 clamp(x, 0, 1))).  Parameters
+ * are exposed like the UNet's for the fp32 restatement test. */
+typedef struct sdx_taesd sdx_taesd;
+int sdx_taesd_create(int imax, uint64_t seed, int device, sdx_taesd** out);
+int sdx_taesd_destroy(sdx_taesd* t);
+int sdx_taesd_encode(sdx_taesd* t, const uint8_t* frames, int n, float* latents, void* stream);
+int sdx_taesd_decode(sdx_taesd* t, const float* latents, int n, uint8_t* frames, void* stream);
+int sdx_taesd_param_count(sdx_taesd* t, int* n);
+int sdx_taesd_param(sdx_taesd* t, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32);
 /* cudaProfilerStart / Stop around a region (for ncu --profile-from-start off). */
 int sdx_profiler_start(void);
 int sdx_profiler_stop(void);

@@ -1353,7 +1353,8 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
         const char* v = std::getenv("SDX_CONV_HALO");
         return !(v && v[0] == '0');
     }();
-    if (halo_on && Cin == 64 && Cout == 64 && stride == 1 && W % 128 == 0 && p.fast && !p.epi.ln_part &&
+    const bool halo_epi_ok = p.fast ? Cout == 64 : (p.epi.n_gn == 0 && !p.epi.geglu);  // narrow heads: general epilogue
+    if (halo_on && Cin == 64 && Cout <= 64 && stride == 1 && W % 128 == 0 && halo_epi_ok && !p.epi.ln_part &&
         !p.epi.row_stats_out && g_force_bn == 0) {
         // halo-tiled: 128-pixel row segments, one 3 x 130 x 64 box per tile, resident weights
         p.amode = kAHalo;
@@ -1375,7 +1376,8 @@ GemmPlan plan_conv3x3(const __nv_bfloat16* x, int imgs, int H, int W, int Cin, c
 void run_gemm(const GemmPlan& p, cudaStream_t st) {
     if (!p.valid) raise(SDX_LOGIC_ERROR, "run_gemm: invalid plan");
     if (p.amode == kAHalo) {
-        launch_t<64, kAHalo, true, false>(p, st);
+        if (p.fast) launch_t<64, kAHalo, true, false>(p, st);
+        else launch_t<64, kAHalo, false, false>(p, st);
         return;
     }
     if (p.fast) {

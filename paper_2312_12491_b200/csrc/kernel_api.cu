@@ -8,7 +8,9 @@
 #include "attention_sm100.cuh"
 #include "gemm_sm100.cuh"
 #include "stagger_b200_kernels.h"
+#include "taesd.cuh"
 #include "unet.cuh"
+#include <numeric>
 #include <vector>
 
 namespace {
@@ -173,6 +175,102 @@ int sdx_kernel_attention_probe(int mode) {
 
 int sdx_kernel_plan_destroy(sdx_gemm_plan* p) {
     return kguard([&] { delete p; });
+}
+
+// ---- TAESD codec on its own (numerics tests / kernel tools) -------------------------
+struct sdx_taesd {
+    sdx::TAESD* t = nullptr;
+    int imax = 0;
+    int *src = nullptr, *dst = nullptr, *enc_cnt = nullptr, *dec_cnt = nullptr;
+    uint8_t *frames_in = nullptr, *frames_out = nullptr;
+    float *lat_out = nullptr, *lat_in = nullptr;
+};
+
+int sdx_taesd_create(int imax, uint64_t seed, int device, sdx_taesd** out) {
+    return kguard([&] {
+        if (imax < 1) sdx::raise(SDX_INVALID_ARGUMENT, "taesd: imax must be >= 1");
+        SDX_CUDA(cudaSetDevice(device));
+        auto* h = new sdx_taesd;
+        h->imax = imax;
+        const size_t fb = 512ull * 512 * 3, lb = 64ull * 64 * 4;
+        h->src = sdx::dev_alloc<int>(imax);
+        h->dst = sdx::dev_alloc<int>(imax);
+        h->enc_cnt = sdx::dev_alloc<int>(1);
+        h->dec_cnt = sdx::dev_alloc<int>(1);
+        h->frames_in = sdx::dev_alloc<uint8_t>(fb * imax);
+        h->frames_out = sdx::dev_alloc<uint8_t>(fb * imax);
+        h->lat_out = sdx::dev_alloc<float>(lb * imax);
+        h->lat_in = sdx::dev_alloc<float>(lb * imax);
+        std::vector<int> iota(static_cast<size_t>(imax));
+        std::iota(iota.begin(), iota.end(), 0);
+        SDX_CUDA(cudaMemcpy(h->src, iota.data(), sizeof(int) * imax, cudaMemcpyHostToDevice));
+        SDX_CUDA(cudaMemcpy(h->dst, iota.data(), sizeof(int) * imax, cudaMemcpyHostToDevice));
+        sdx::TaesdIO io;
+        io.frames = h->frames_in;
+        io.frame_stride = static_cast<long long>(fb);
+        io.enc_src = h->src;
+        io.enc_count = h->enc_cnt;
+        io.latent_out = h->lat_out;
+        io.enc_dst = h->dst;
+        io.latent_in = h->lat_in;
+        io.dec_src = h->src;
+        io.dec_count = h->dec_cnt;
+        io.frames_out = h->frames_out;
+        io.dec_dst = h->dst;
+        h->t = new sdx::TAESD(imax, seed, io, nullptr);
+        *out = h;
+    });
+}
+
+int sdx_taesd_destroy(sdx_taesd* h) {
+    return kguard([&] {
+        if (!h) return;
+        delete h->t;
+        for (void* p : {static_cast<void*>(h->src), static_cast<void*>(h->dst), static_cast<void*>(h->enc_cnt),
+                        static_cast<void*>(h->dec_cnt), static_cast<void*>(h->frames_in),
+                        static_cast<void*>(h->frames_out), static_cast<void*>(h->lat_out), static_cast<void*>(h->lat_in)})
+            sdx::dev_free(p);
+        delete h;
+    });
+}
+
+int sdx_taesd_encode(sdx_taesd* h, const uint8_t* frames, int n, float* latents, void* stream) {
+    return kguard([&] {
+        if (!h || n < 1 || n > h->imax) sdx::raise(SDX_INVALID_ARGUMENT, "taesd_encode: 1 <= n <= imax");
+        auto st = static_cast<cudaStream_t>(stream);
+        SDX_CUDA(cudaMemcpyAsync(h->frames_in, frames, 512ull * 512 * 3 * n, cudaMemcpyDeviceToDevice, st));
+        SDX_CUDA(cudaMemcpyAsync(h->enc_cnt, &n, sizeof(int), cudaMemcpyHostToDevice, st));
+        h->t->encode(st);
+        SDX_CUDA(cudaMemcpyAsync(latents, h->lat_out, 64ull * 64 * 4 * sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+        SDX_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int sdx_taesd_decode(sdx_taesd* h, const float* latents, int n, uint8_t* frames, void* stream) {
+    return kguard([&] {
+        if (!h || n < 1 || n > h->imax) sdx::raise(SDX_INVALID_ARGUMENT, "taesd_decode: 1 <= n <= imax");
+        auto st = static_cast<cudaStream_t>(stream);
+        SDX_CUDA(cudaMemcpyAsync(h->lat_in, latents, 64ull * 64 * 4 * sizeof(float) * n, cudaMemcpyDeviceToDevice, st));
+        SDX_CUDA(cudaMemcpyAsync(h->dec_cnt, &n, sizeof(int), cudaMemcpyHostToDevice, st));
+        h->t->decode(st);
+        SDX_CUDA(cudaMemcpyAsync(frames, h->frames_out, 512ull * 512 * 3 * n, cudaMemcpyDeviceToDevice, st));
+        SDX_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int sdx_taesd_param_count(sdx_taesd* h, int* n) {
+    return kguard([&] { *n = static_cast<int>(h->t->params().size()); });
+}
+
+int sdx_taesd_param(sdx_taesd* h, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32) {
+    return kguard([&] {
+        const auto& p = h->t->params().at(static_cast<size_t>(i));
+        *name = p.name.c_str();
+        *ptr = p.ptr;
+        *ndim = static_cast<int>(p.shape.size());
+        for (size_t k = 0; k < p.shape.size() && k < 4; ++k) shape[k] = p.shape[k];
+        *is_f32 = p.f32 ? 1 : 0;
+    });
 }
 
 struct sdx_unet {

@@ -395,6 +395,67 @@ __global__ void im2col_kernel(const T* __restrict__ in, long long img_stride, co
     }
 }
 
+// ---- direct 3x3 conv of u8 RGB frames (the TAESD encoder's first layer) -------------
+// One thread = one output pixel x 64 channels on CUDA cores: the 27 inputs (3 rows
+// of 3 pixels x 3 channels, u8 / 255, zero padding) come from a shared row tile,
+// weights [64][K>=27] (column k = tap * 3 + c, as the im2col layout) are staged in smem
+// as fp32 [27][64] and read as broadcast float4s.  Replaces im2col (a 64-column bf16
+// matrix per pixel) + GEMM.
+__global__ void __launch_bounds__(256) conv3x3_rgb8_kernel(const uint8_t* __restrict__ in, long long img_stride,
+                                                           const int* img_src, int H, int W, const bf16* __restrict__ w,
+                                                           int ldw, const float* __restrict__ bias,
+                                                           bf16* __restrict__ out, const int* rows_dev) {
+    pdl_launch();
+    pdl_wait();
+    const int n = blockIdx.z, y = blockIdx.y, x0 = blockIdx.x * 256;
+    if (rows_dev && n >= *rows_dev) return;
+    __shared__ __align__(16) float ws[27][64];
+    __shared__ float bs[64];
+    __shared__ uint8_t rowt[3][258 * 3];
+    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) {
+        const int k = i / 64, co = i % 64;
+        ws[k][co] = __bfloat162float(w[static_cast<long long>(co) * ldw + k]);
+    }
+    if (threadIdx.x < 64) bs[threadIdx.x] = bias ? bias[threadIdx.x] : 0.f;
+    const uint8_t* base = in + static_cast<long long>(img_src ? img_src[n] : n) * img_stride;
+    for (int i = threadIdx.x; i < 3 * 258 * 3; i += blockDim.x) {
+        const int r = i / (258 * 3), rem = i % (258 * 3);
+        const int xx = x0 - 1 + rem / 3, yy = y - 1 + r;
+        rowt[r][rem] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? base[(static_cast<long long>(yy) * W + xx) * 3 + rem % 3] : 0;
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x;
+    if (x >= W) return;
+    float v[27];
+#pragma unroll
+    for (int dy = 0; dy < 3; ++dy)
+#pragma unroll
+        for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                v[(dy * 3 + dx) * 3 + c] = static_cast<float>(rowt[dy][(threadIdx.x + dx) * 3 + c]) * (1.f / 255.f);
+    bf16* op = out + ((static_cast<long long>(n) * H + y) * W + x) * 64;
+#pragma unroll
+    for (int cb = 0; cb < 64; cb += 16) {
+        float acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = bs[cb + i];
+#pragma unroll
+        for (int k = 0; k < 27; ++k) {
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+                const float4 wv = *reinterpret_cast<const float4*>(&ws[k][cb + i]);
+                acc[i] = fmaf(v[k], wv.x, acc[i]);
+                acc[i + 1] = fmaf(v[k], wv.y, acc[i + 1]);
+                acc[i + 2] = fmaf(v[k], wv.z, acc[i + 2]);
+                acc[i + 3] = fmaf(v[k], wv.w, acc[i + 3]);
+            }
+        }
+        store8(op + cb, acc);
+        store8(op + cb + 8, acc + 8);
+    }
+}
+
 // ---- timestep embedding ------------------------------------------------------------
 
 __global__ void temb_kernel(const int* taus, int n, int dim, bf16* out) {
@@ -569,6 +630,13 @@ void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_sr
                       int Kp, bf16* out, const int* rows_dev, cudaStream_t st) {
     launch_pdl(im2col_kernel<uint8_t>, dim3(grid_for(static_cast<long long>(imgs) * H * W * Kp / 8, 256)), dim3(256), 0,
                st, in, img_stride, img_src, imgs, H, W, C, Kp, 1.f / 255.f, 0, out, rows_dev);
+}
+
+void run_conv3x3_rgb8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W,
+                      const bf16* w, int ldw, const float* bias, bf16* out, const int* rows_dev, cudaStream_t st) {
+    if (ldw < 27) raise(SDX_INVALID_ARGUMENT, "conv3x3_rgb8: weight row shorter than 27");
+    launch_pdl(conv3x3_rgb8_kernel, dim3((W + 255) / 256, H, imgs), dim3(256), 0, st, in, img_stride, img_src, H, W, w,
+               ldw, bias, out, rows_dev);
 }
 
 void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStream_t st) {

@@ -59,6 +59,11 @@ void run_im2col3x3_f32_gather(const float* in, long long img_stride, const int* 
 void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W, int C,
                       int Kp, bf16* out, const int* rows_dev, cudaStream_t st);
 
+// Direct 3x3 / pad 1 conv of u8 NHWC RGB frames (scaled 1/255) to 64 bf16 channels:
+// w [64][ldw] bf16 with column k = tap * 3 + c (k < 27), bias [64] or null.
+void run_conv3x3_rgb8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W,
+                      const bf16* w, int ldw, const float* bias, bf16* out, const int* rows_dev, cudaStream_t st);
+
 // sinusoidal timestep embedding (flip_sin_to_cos, shift 0): [n][dim] bf16
 void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStream_t st);
 

@@ -64,29 +64,24 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             bufs_[r][k] = dev_alloc<bf16>(static_cast<size_t>(imax) * kRes[r] * kRes[r] * kC);
             allocs_.push_back(bufs_[r][k]);
         }
-    a0_ = dev_alloc<bf16>(static_cast<size_t>(imax) * 512 * 512 * 64);
+    a0_ = dev_alloc<bf16>(static_cast<size_t>(imax) * 64 * 64 * 64);  // decoder conv_in im2col (64x64 latents)
     allocs_.push_back(a0_);
 
     // ---------------- encoder ----------------
     if (io.frames) {
         const int* cnt = io.enc_count;
         {
+            // first layer (3 -> 64) as a direct CUDA-core conv of the u8 frames
+            const float* b = wf32("enc.conv_in.b", {kC}, 0.02f);
+            const bf16* w = wbf("enc.conv_in.w", {kC, 64}, std::sqrt(2.f / 27.f));  // cols >= 27 unused
             const uint8_t* fr = io.frames;
             const long long fs = io.frame_stride;
             const int* src = io.enc_src;
             const int im = imax_;
-            bf16* a0 = a0_;
-            enc_.push_back(Op{"im2col", [=](cudaStream_t s) { run_im2col3x3_u8(fr, fs, src, im, 512, 512, 3, 64, a0, cnt, s); }});
-        }
-        {
-            GemmEpilogue e;
-            e.bias = wf32("enc.conv_in.b", {kC}, 0.02f);
-            e.out = buf(0, 0);
-            e.rows_dev = cnt;
-            e.rows_per_unit = 512 * 512;
-            bf16* w = wbf("enc.conv_in.w", {kC, 64}, std::sqrt(2.f / 27.f));  // cols >= 27 multiply zero padding
-            GemmPlan p = plan_gemm(a0_, 64, w, 64, imax_ * 512 * 512, kC, 64, e);
-            enc_.push_back(Op{"conv_in", [p](cudaStream_t s) { run_gemm(p, s); }});
+            bf16* o = buf(0, 0);
+            enc_.push_back(Op{"conv_in", [=](cudaStream_t s) {
+                                  run_conv3x3_rgb8(fr, fs, src, im, 512, 512, w, 64, b, o, cnt, s);
+                              }});
             enc_flops_ += 2.0 * 512 * 512 * kC * 27;
         }
         int cur = block(enc_, enc_flops_, 0, 0, "enc.b0", cnt);
