@@ -102,6 +102,7 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
     const long long M = static_cast<long long>(R_) * HW;
     const int Cin = Cx + (skip ? Cs : 0);
     const int* rows = rows_dev_;
+    const size_t fork_at = ops_.size();  // the shortcut GEMM (if any) forks off here
     // norm1 + SiLU over [x | skip]
     bf16* t1 = act(M * Cin);
     {
@@ -152,6 +153,27 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
         if (skip) gemm_op("conv1x1", plan_gemm_concat(x, Cx, Cx, skip, Cs, w, Cin, static_cast<int>(M), Cout, Cin, e));
         else gemm_op("conv1x1", plan_gemm(x, Cx, w, Cin, static_cast<int>(M), Cout, Cin, e));
         shortcut = s;
+        // The shortcut depends only on the block input: run it on the side stream from the
+        // start of the block (graph branch), concurrent with GN1 -> conv1 -> GN2, and join
+        // before conv2, which adds it as the residual.
+        Op sc = ops_.back();
+        ops_.pop_back();
+        cudaEvent_t ea, eb;
+        SDX_CUDA(cudaEventCreateWithFlags(&ea, cudaEventDisableTiming));
+        SDX_CUDA(cudaEventCreateWithFlags(&eb, cudaEventDisableTiming));
+        fork_events_.push_back(ea);
+        fork_events_.push_back(eb);
+        cudaStream_t side = side_;
+        auto inner = sc.fn;
+        sc.fn = [=](cudaStream_t st) {
+            SDX_CUDA(cudaEventRecord(ea, st));
+            SDX_CUDA(cudaStreamWaitEvent(side, ea, 0));
+            inner(side);
+            SDX_CUDA(cudaEventRecord(eb, side));
+        };
+        sc.join = [=](cudaStream_t st) { SDX_CUDA(cudaStreamWaitEvent(st, eb, 0)); };
+        ops_.insert(ops_.begin() + static_cast<long>(fork_at), sc);
+        ops_.push_back(Op{"join", [=](cudaStream_t st) { SDX_CUDA(cudaStreamWaitEvent(st, eb, 0)); }, "join", 0.0, nullptr});
     }
     bf16* out = act(M * Cout);
     {
@@ -345,6 +367,7 @@ bf16* UNet::upsample(const bf16* x, int C, int H, int W, const std::string& nm) 
 UNet::UNet(const UNetConfig& cfg, cudaStream_t st) : cfg_(cfg) {
     R_ = cfg.rmax;
     const int H = cfg.H, W = cfg.W;
+    SDX_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
     const int n_steps = static_cast<int>(cfg.taus.size());
     if (n_steps < 1) raise(SDX_INVALID_ARGUMENT, "UNet: empty schedule");
     SDX_CUDA(cudaDeviceSynchronize());
@@ -495,6 +518,8 @@ UNet::UNet(const UNetConfig& cfg, cudaStream_t st) : cfg_(cfg) {
 
 UNet::~UNet() {
     cudaDeviceSynchronize();
+    for (auto e : fork_events_) cudaEventDestroy(e);
+    if (side_) cudaStreamDestroy(side_);
     for (auto& g : gns_) free_groupnorm(g);
     for (void* p : allocs_) dev_free(p);
 }
@@ -534,10 +559,17 @@ void UNet::forward_profiled(const int* rows_dev, cudaStream_t, std::vector<std::
     SDX_CUDA(cudaStreamSynchronize(cs));
     out->clear();
     for (size_t i = 0; i < ops_.size(); ++i) {
+        if (ops_[i].kind == "join") {
+            out->push_back({ops_[i].kind, 0.f});
+            continue;
+        }
         cudaGraph_t graph = nullptr;
         cudaGraphExec_t exec = nullptr;
         SDX_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-        for (int r = 0; r < kReps; ++r) ops_[i].fn(cs);
+        for (int r = 0; r < kReps; ++r) {
+            ops_[i].fn(cs);
+            if (ops_[i].join) ops_[i].join(cs);
+        }
         SDX_CUDA(cudaStreamEndCapture(cs, &graph));
         SDX_CUDA(cudaGraphInstantiate(&exec, graph, 0));
         SDX_CUDA(cudaGraphLaunch(exec, cs));

@@ -64,7 +64,11 @@ class UNet {
     void forward(const int* rows_dev, cudaStream_t st);
     const std::vector<Param>& params() const { return params_; }
     double flops_per_row() const { return flops_per_row_; }
-    int launches_per_forward() const { return static_cast<int>(ops_.size()); }
+    int launches_per_forward() const {
+        int n = 0;
+        for (const auto& op : ops_) n += op.kind != "join";
+        return n;
+    }
     const UNetConfig& config() const { return cfg_; }
     // Device time of each op class accumulated by forward_profiled (ms).
     void forward_profiled(const int* rows_dev, cudaStream_t st, std::vector<std::pair<std::string, float>>* out);
@@ -78,7 +82,12 @@ class UNet {
         std::function<void(cudaStream_t)> fn;
         std::string label;   // kind + shape (profiling)
         double flops = 0;    // algorithmic FLOPs at rmax rows (tensor ops)
+        // forked ops (fn runs on the side stream): rejoins the caller's stream when the op is
+        // run on its own (per-op profile); in the forward a separate "join" op does that
+        std::function<void(cudaStream_t)> join;
     };
+    cudaStream_t side_ = nullptr;           // resblock shortcut GEMMs run here, concurrent with GN/conv1/GN
+    std::vector<cudaEvent_t> fork_events_;
     bf16* wbf(const std::string& name, std::vector<long long> shape, float std);
     float* wf32(const std::string& name, std::vector<long long> shape, float std, float constant);
     bf16* act(long long elems);
