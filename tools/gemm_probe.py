@@ -45,6 +45,12 @@ def gemm(M, N, K, bn, s=1):
                                             0, bn, s, hp), 2.0 * M * N * K)
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "bn":
+    for bn in (64, 96, 128, 160, 192, 224, 256, -128, -160, -256):
+        gemm(8192, 8192, 4096, bn)
+    for bn in (64, 128, 160, 192, 256, -256):
+        conv(8, 64, 640, 640, bn)
+    sys.exit(0)
 for bn in (160, 192, 256, -160, -256):
     conv(4, 64, 320, 320, bn)
 for bn in (160, 256, -256):
