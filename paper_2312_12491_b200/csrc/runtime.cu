@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 
@@ -512,12 +513,30 @@ Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const 
         io.enc_count = lists_.n_ingest;
         io.latent_out = dev_.x0;
         io.enc_dst = lists_.enc_dst;
-        io.latent_in = dev_.emitted;
-        io.dec_src = lists_.dec_src;
-        io.dec_count = lists_.n_emit;
+        // the decoder reads its own copy of the emitted latents and codec lists
+        // (staged per ring slot by the main part of the iteration)
+        const int nl = 4 * S_ + 2;
+        stage_lat_ = dev_alloc<float>(static_cast<size_t>(K_) * S_ * d);
+        stage_lists_ = dev_alloc<int>(static_cast<size_t>(K_) * nl);
+        dec_in_ = dev_alloc<float>(static_cast<size_t>(S_) * d);
+        dec_lists_ = dev_alloc<int>(static_cast<size_t>(nl));
+        SDX_CUDA(cudaMemset(stage_lists_, 0, sizeof(int) * K_ * nl));
+        SDX_CUDA(cudaMemset(dec_lists_, 0, sizeof(int) * nl));
+        io.latent_in = dec_in_;
+        io.dec_src = dec_lists_ + 2 * S_;
+        io.dec_count = dec_lists_ + 4 * S_ + 1;
         io.frames_out = d_out_;
-        io.dec_dst = lists_.dec_dst;
+        io.dec_dst = dec_lists_ + 3 * S_;
+        const char* ov = std::getenv("SDX_DECODE_OVERLAP");
+        overlap_ = !(ov && ov[0] == '0');
+        io.separate_decoder_buffers = overlap_;
         taesd_ = std::make_unique<TAESD>(S_, e.seed ^ 0x7AE5DULL, io, stream_);
+        if (overlap_) {
+            SDX_CUDA(cudaStreamCreateWithFlags(&dec_stream_, cudaStreamNonBlocking));
+            main_done_.resize(static_cast<size_t>(K_));
+            for (auto& ev : main_done_) SDX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            SDX_CUDA(cudaEventCreateWithFlags(&dec_join_, cudaEventDisableTiming));
+        }
     }
     SDX_CUDA(cudaMallocHost(&h_in_, static_cast<size_t>(K_) * S_ * D_));
     SDX_CUDA(cudaMallocHost(&h_out_, static_cast<size_t>(K_) * S_ * out_bytes_));
@@ -538,12 +557,22 @@ Pipeline::~Pipeline() {
     cudaSetDevice(device_);
     if (stream_) cudaStreamSynchronize(stream_);
     if (copy_) cudaStreamSynchronize(copy_);
+    if (dec_stream_) cudaStreamSynchronize(dec_stream_);
     for (auto gexec : graphs_)
+        if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto gexec : dec_graphs_)
         if (gexec) cudaGraphExecDestroy(gexec);
     taesd_.reset();
     unet_.reset();
     dev_free(lists_buf_);
     dev_free(d_out_);
+    dev_free(stage_lat_);
+    dev_free(stage_lists_);
+    dev_free(dec_in_);
+    dev_free(dec_lists_);
+    for (auto ev : main_done_) cudaEventDestroy(ev);
+    if (dec_join_) cudaEventDestroy(dec_join_);
+    if (dec_stream_) cudaStreamDestroy(dec_stream_);
     dev_.release();
     dev_free(d_in_);
     dev_free(d_ref_);
@@ -631,18 +660,43 @@ void Pipeline::launch_iteration(int k, bool frame_present) {
     launches_ += 2;
     mark(5);
     if (taesd) {
-        taesd_->decode(stream_);
-        launches_ += taesd_->launches_per_decode();
+        // stage this slot's emitted latents and codec lists for its decode
+        const int nl = 4 * S_ + 2;
+        SDX_CUDA(cudaMemcpyAsync(stage_lat_ + static_cast<size_t>(k) * S_ * d_, dev_.emitted,
+                                 sizeof(float) * S_ * d_, cudaMemcpyDeviceToDevice, stream_));
+        SDX_CUDA(cudaMemcpyAsync(stage_lists_ + static_cast<size_t>(k) * nl, lists_buf_, sizeof(int) * nl,
+                                 cudaMemcpyDeviceToDevice, stream_));
+        if (!(overlap_ && !profile_)) launch_decode(k, stream_);
     }
     mark(6);
     SDX_CUDA(cudaMemcpyAsync(h_log_ + static_cast<size_t>(k) * S_, dev_.log, sizeof(LogEntry) * S_,
                              cudaMemcpyDeviceToHost, stream_));
-    if (!resident_ || copy_outputs_) {
-        const void* src = taesd ? static_cast<const void*>(d_out_ + static_cast<size_t>(k) * S_ * out_bytes_)
-                                : static_cast<const void*>(dev_.emitted);
-        SDX_CUDA(cudaMemcpyAsync(h_out_ + static_cast<size_t>(k) * S_ * out_bytes_, src, out_bytes_ * S_,
+    if (!taesd && (!resident_ || copy_outputs_))
+        SDX_CUDA(cudaMemcpyAsync(h_out_ + static_cast<size_t>(k) * S_ * out_bytes_, dev_.emitted, out_bytes_ * S_,
                                  cudaMemcpyDeviceToHost, stream_));
-    }
+}
+
+// Decode of ring slot k (TAESD codec): the staged latents and lists into the
+// decoder's inputs, the decoder, the frames back to the host.
+void Pipeline::launch_decode(int k, cudaStream_t s) {
+    const int nl = 4 * S_ + 2;
+    SDX_CUDA(cudaMemcpyAsync(dec_in_, stage_lat_ + static_cast<size_t>(k) * S_ * d_, sizeof(float) * S_ * d_,
+                             cudaMemcpyDeviceToDevice, s));
+    SDX_CUDA(cudaMemcpyAsync(dec_lists_, stage_lists_ + static_cast<size_t>(k) * nl, sizeof(int) * nl,
+                             cudaMemcpyDeviceToDevice, s));
+    taesd_->decode(s);
+    launches_ += taesd_->launches_per_decode();
+    if (!resident_ || copy_outputs_)
+        SDX_CUDA(cudaMemcpyAsync(h_out_ + static_cast<size_t>(k) * S_ * out_bytes_,
+                                 d_out_ + static_cast<size_t>(k) * S_ * out_bytes_, out_bytes_ * S_,
+                                 cudaMemcpyDeviceToHost, s));
+}
+
+// Make stream_ wait for every decode issued so far (timer marks, sync).
+void Pipeline::join_decode() {
+    if (!dec_stream_) return;
+    SDX_CUDA(cudaEventRecord(dec_join_, dec_stream_));
+    SDX_CUDA(cudaStreamWaitEvent(stream_, dec_join_, 0));
 }
 
 // One iteration on ring slot k: wait for the slot's H2D, run the iteration
@@ -673,7 +727,36 @@ void Pipeline::run_iteration(int k, bool frame_present) {
         SDX_CUDA(cudaGraphLaunch(graphs_[static_cast<size_t>(key)], stream_));
         launches_ += graph_launches_[static_cast<size_t>(key)];
     }
-    SDX_CUDA(cudaEventRecord(done_[static_cast<size_t>(k)], stream_));
+    if (taesd_ && overlap_ && !profile_) {
+        // the decode of slot k overlaps the next iteration's main part
+        SDX_CUDA(cudaEventRecord(main_done_[static_cast<size_t>(k)], stream_));
+        SDX_CUDA(cudaStreamWaitEvent(dec_stream_, main_done_[static_cast<size_t>(k)], 0));
+        if (!cfg_.graph) {
+            launch_decode(k, dec_stream_);
+        } else {
+            const int key = k * 2 + ((!resident_ || copy_outputs_) ? 1 : 0);
+            if (dec_graphs_.size() < static_cast<size_t>(2 * K_)) {
+                dec_graphs_.assign(static_cast<size_t>(2 * K_), nullptr);
+                dec_graph_launches_.assign(static_cast<size_t>(2 * K_), 0);
+            }
+            if (!dec_graphs_[static_cast<size_t>(key)]) {
+                const long long before = launches_;
+                cudaGraph_t g = nullptr;
+                SDX_CUDA(cudaStreamBeginCapture(dec_stream_, cudaStreamCaptureModeThreadLocal));
+                launch_decode(k, dec_stream_);
+                SDX_CUDA(cudaStreamEndCapture(dec_stream_, &g));
+                SDX_CUDA(cudaGraphInstantiate(&dec_graphs_[static_cast<size_t>(key)], g, 0));
+                SDX_CUDA(cudaGraphDestroy(g));
+                dec_graph_launches_[static_cast<size_t>(key)] = launches_ - before;
+                launches_ = before;
+            }
+            SDX_CUDA(cudaGraphLaunch(dec_graphs_[static_cast<size_t>(key)], dec_stream_));
+            launches_ += dec_graph_launches_[static_cast<size_t>(key)];
+        }
+        SDX_CUDA(cudaEventRecord(done_[static_cast<size_t>(k)], dec_stream_));
+    } else {
+        SDX_CUDA(cudaEventRecord(done_[static_cast<size_t>(k)], stream_));
+    }
 }
 
 std::shared_ptr<std::vector<uint8_t>> Pipeline::acquire_buffer() {
@@ -945,11 +1028,13 @@ const std::string& Pipeline::error(int stream) const { return st_[static_cast<si
 void Pipeline::sync() {
     SDX_CUDA(cudaSetDevice(device_));
     drain_completed(true);
+    join_decode();
     SDX_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void Pipeline::reset_timer() {
     SDX_CUDA(cudaSetDevice(device_));
+    join_decode();
     SDX_CUDA(cudaEventRecord(t0_, stream_));
 }
 
@@ -973,6 +1058,7 @@ void Pipeline::stage_times(double* ms, long long* iters) const {
 
 float Pipeline::device_time_ms() {
     SDX_CUDA(cudaSetDevice(device_));
+    join_decode();
     SDX_CUDA(cudaEventRecord(t1_, stream_));
     SDX_CUDA(cudaEventSynchronize(t1_));
     float ms = 0.f;

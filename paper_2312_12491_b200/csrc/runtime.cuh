@@ -186,7 +186,9 @@ class Pipeline {
         std::string error;
     };
     void launch_iteration(int k, bool frame_present);
+    void launch_decode(int k, cudaStream_t s);
     void run_iteration(int k, bool frame_present);
+    void join_decode();
     void process(int k, bool frame_present);
     std::vector<cudaGraphExec_t> graphs_;     // [ring slot][output-copy variant]
     std::vector<long long> graph_launches_;
@@ -228,6 +230,21 @@ class Pipeline {
     int* lists_buf_ = nullptr;
     CodecLists lists_{};
     uint8_t* d_out_ = nullptr;  // [K][S][frame_bytes] decoded frames (TAESD)
+    // Decode overlap (TAESD codec): iteration t's decode runs on dec_stream_
+    // while iteration t+1's SSF / encode / UNet / step run on stream_.  The
+    // main graph stages the emitted latents and codec lists per ring slot; the
+    // decode graph copies them into the decoder's fixed inputs, decodes, and
+    // reads the frames back; done_[k] is recorded after it.
+    bool overlap_ = false;
+    cudaStream_t dec_stream_ = nullptr;
+    std::vector<cudaEvent_t> main_done_;  // [K] main part of slot k finished
+    cudaEvent_t dec_join_ = nullptr;
+    float* stage_lat_ = nullptr;   // [K][S][d] emitted latents
+    int* stage_lists_ = nullptr;   // [K][4S+2] codec lists
+    float* dec_in_ = nullptr;      // [S][d] decoder input
+    int* dec_lists_ = nullptr;     // [4S+2]
+    std::vector<cudaGraphExec_t> dec_graphs_;  // [ring slot][output-copy variant]
+    std::vector<long long> dec_graph_launches_;
 };
 
 }  // namespace sdx

@@ -59,11 +59,17 @@ int TAESD::block(std::vector<Op>& ops, double& flops, int r, int in, const std::
 }
 
 TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax_(imax), seed_(seed) {
-    for (int r = 0; r < 4; ++r)
-        for (int k = 0; k < 3; ++k) {
-            bufs_[r][k] = dev_alloc<bf16>(static_cast<size_t>(imax) * kRes[r] * kRes[r] * kC);
-            allocs_.push_back(bufs_[r][k]);
-        }
+    const int sets = io.separate_decoder_buffers && io.frames && io.latent_in ? 2 : 1;
+    for (int set = 0; set < 2; ++set)
+        for (int r = 0; r < 4; ++r)
+            for (int k = 0; k < 3; ++k) {
+                if (set < sets) {
+                    bufs_[set][r][k] = dev_alloc<bf16>(static_cast<size_t>(imax) * kRes[r] * kRes[r] * kC);
+                    allocs_.push_back(bufs_[set][r][k]);
+                } else {
+                    bufs_[set][r][k] = bufs_[0][r][k];
+                }
+            }
     a0_ = dev_alloc<bf16>(static_cast<size_t>(imax) * 64 * 64 * 64);  // decoder conv_in im2col (64x64 latents)
     allocs_.push_back(a0_);
 
@@ -107,6 +113,7 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
         }
     }
     // ---------------- decoder ----------------
+    set_ = 1;
     if (io.latent_in) {
         const int* cnt = io.dec_count;
         {
@@ -161,6 +168,7 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             dec_flops_ += 2.0 * 512 * 512 * 3 * 9.0 * kC;
         }
     }
+    set_ = 0;
     SDX_CUDA(cudaStreamSynchronize(st));
     SDX_CUDA(cudaDeviceSynchronize());
 }

@@ -41,6 +41,9 @@ struct TaesdIO {
     const int* dec_count = nullptr;
     uint8_t* frames_out = nullptr;     // [.][512*512*3] u8
     const int* dec_dst = nullptr;
+    // decoder activations in their own buffers, so a decode may run on another
+    // stream concurrently with the next encode
+    bool separate_decoder_buffers = false;
 };
 
 class TAESD {
@@ -68,13 +71,14 @@ class TAESD {
               int act, const bf16* residual, bf16* out, const int* count);
     // returns the buffer index holding the output
     int block(std::vector<Op>& ops, double& flops, int res_idx, int in, const std::string& nm, const int* count);
-    bf16* buf(int res_idx, int k) { return bufs_[res_idx][k]; }
+    bf16* buf(int res_idx, int k) { return bufs_[set_][res_idx][k]; }
 
     int imax_;
     uint64_t seed_, counter_ = 0;
     std::vector<Param> params_;
     std::vector<void*> allocs_;
-    bf16* bufs_[4][3];  // resolutions 512, 256, 128, 64
+    bf16* bufs_[2][4][3] = {};  // [encoder, decoder][resolution 512, 256, 128, 64][3]
+    int set_ = 0;
     bf16* a0_ = nullptr;  // im2col scratch [imax*512*512][64]
     std::vector<Op> enc_, dec_;
     double enc_flops_ = 0, dec_flops_ = 0;
