@@ -30,6 +30,14 @@ int sdx_kernel_conv3x3(const void* x, int imgs, int H, int W, int Cin, const voi
                        const float* bias, const float* bias_img, const void* residual, int act, void* out,
                        int out_f32, void* stream);
 
+/* GroupNorm (32 groups) over NHWC bf16, optionally over the channel concat
+ * [x1 | x2] (decoder skip joins), + SiLU when silu != 0; fp32 affine gamma/beta.
+ * arena: device scratch of imgs*64 + 1 u64 (zeroed here before every pass).
+ * iters > 1 repeats the pass (zero + statistics + apply) for timing. */
+int sdx_kernel_groupnorm(const void* x1, int C1, const void* x2, int C2, int HW, int imgs, float eps,
+                         const float* gamma, const float* beta, int silu, void* out, void* arena, int iters,
+                         void* stream);
+
 /* Flash attention, head_dim 64, tcgen05: out[img*q_len + i][64h..] = softmax(q k^T * scale) v
  * per (image, head).  Q rows [images*q_len][ld_q] (head h at q_col0 + 64h); KV rows
  * [kv_rows_total][ld_kv] with K at k_col0 + 64h and V at v_col0 + 64h; image i reads

@@ -418,6 +418,14 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                 const float var = fmaxf(s2 * inv_c - ln_mean * ln_mean, 0.f);
                 ln_rstd = rsqrtf(var + g.epi.ln_eps);
             }
+            // residual: the first chunk's row segment is requested before waiting for
+            // the accumulator (its latency hides under this tile's MMAs)
+            const __nv_bfloat16* res_row = e_res ? e_res + static_cast<long long>(row < m_eff ? row : 0) * e_ldres : nullptr;
+            uint4 rq[4];
+            if (res_row && n0 + part * 32 < g.N) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) rq[i] = reinterpret_cast<const uint4*>(res_row + n0 + part * 32)[i];
+            }
             wait_bounded(&tfull[acc], (lt >> 1) & 1);
             if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[4] = gtimer();
             tc_fence_after();
@@ -428,11 +436,9 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
             for (int c = part * 32; c < BN; c += CSTEP, ++kc) {
                 const int col0 = n0 + c;
                 if (col0 >= g.N) break;  // warp-uniform; N % 32 == 0 on this path
-                uint4 rq[4];
-                if (e_res) {
-                    const uint4* rp = reinterpret_cast<const uint4*>(e_res + static_cast<long long>(row < m_eff ? row : 0) * e_ldres + col0);
+                if (res_row && kc > 0) {
 #pragma unroll
-                    for (int i = 0; i < 4; ++i) rq[i] = rp[i];
+                    for (int i = 0; i < 4; ++i) rq[i] = reinterpret_cast<const uint4*>(res_row + col0)[i];
                 }
                 uint32_t r[32];
                 tmem_ld32_nowait(tbase + c, r);

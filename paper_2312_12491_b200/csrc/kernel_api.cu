@@ -2,6 +2,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -82,6 +83,33 @@ int sdx_kernel_conv3x3(const void* x, int imgs, int H, int W, int Cin, const voi
         auto p = sdx::plan_conv3x3(static_cast<const bf16*>(x), imgs, H, W, Cin, static_cast<const bf16*>(w), Cout,
                                    stride, e);
         sdx::run_gemm(p, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int sdx_kernel_groupnorm(const void* x1, int C1, const void* x2, int C2, int HW, int imgs, float eps,
+                         const float* gamma, const float* beta, int silu, void* out, void* arena, int iters,
+                         void* stream) {
+    return kguard([&] {
+        if (!arena || imgs < 1 || HW < 1 || iters < 1) sdx::raise(SDX_INVALID_ARGUMENT, "groupnorm: bad arguments");
+        auto* acc = static_cast<unsigned long long*>(arena);
+        auto p = sdx::plan_groupnorm(static_cast<const bf16*>(x1), C1, static_cast<const bf16*>(x2), C2, HW, imgs, eps,
+                                     gamma, beta, silu, static_cast<bf16*>(out), nullptr, acc,
+                                     acc + static_cast<long long>(imgs) * 64);
+        const auto st = static_cast<cudaStream_t>(stream);
+        // timing breakdown knob (tools/gn_bench.py): bit 0 zero, bit 1 statistics, bit 2 apply
+        const char* pe = std::getenv("SDX_GN_PARTS");
+        const int parts = pe ? std::atoi(pe) : 7;
+        for (int i = 0; i < iters; ++i) {
+            if (parts & 1)
+                SDX_CUDA(cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * (static_cast<size_t>(imgs) * 64 + 1), st));
+            if ((parts & 6) == 6) {
+                sdx::run_groupnorm(p, st);
+            } else if (parts & 6) {
+                auto q = p;
+                q.stats_fused = (parts & 2) ? 0 : 1;
+                sdx::run_groupnorm_part(q, (parts & 2) ? 0 : 1, st);
+            }
+        }
     });
 }
 

@@ -3,9 +3,12 @@
 // im2col, timestep embedding, initialisers.  All vectorised over 8 bf16
 // channels (16 B) of NHWC activations; statistics in fp32.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "nn_kernels.cuh"
@@ -22,6 +25,61 @@ __device__ __forceinline__ void load8(const bf16* p, float* v) {
         const float2 f = __bfloat1622float2(h[i]);
         v[2 * i] = f.x;
         v[2 * i + 1] = f.y;
+    }
+}
+
+__device__ __forceinline__ void unpack8(const uint4& u, float* v) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float2 f = __bfloat1622float2(h[i]);
+        v[2 * i] = f.x;
+        v[2 * i + 1] = f.y;
+    }
+}
+
+// GroupNorm statistics of one octet: per-channel sum and sum of squares (3
+// instructions per value; the split into the octet's <= 2 groups is done once).
+__device__ __forceinline__ void gn_acc8(const uint4& u, float* as, float* aq) {
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float lo = __uint_as_float(w[i] << 16), hi = __uint_as_float(w[i] & 0xffff0000u);
+        as[2 * i] += lo;
+        aq[2 * i] = fmaf(lo, lo, aq[2 * i]);
+        as[2 * i + 1] += hi;
+        aq[2 * i + 1] = fmaf(hi, hi, aq[2 * i + 1]);
+    }
+}
+__device__ __forceinline__ void gn_split8(const float* as, const float* aq, int split, float& s0, float& q0, float& s1,
+                                          float& q1) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        if (i < split) {
+            s0 += as[i];
+            q0 += aq[i];
+        } else {
+            s1 += as[i];
+            q1 += aq[i];
+        }
+    }
+}
+
+// y = GN(x) -> (SiLU) for 8 values: SiLU(y) = y * (0.5 + 0.5 tanh(y / 2)) with one
+// packed tanh.approx.f16x2 per 2 values (the SFU pipe, 16 ops/clk/SM, bounds the
+// apply pass with exp + reciprocal); |rel err| ~1e-3, below the bf16 output rounding.
+__device__ __forceinline__ void gn_affine8(float* v, const float* sc, const float* sh, int silu) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = fmaf(v[i], sc[i], sh[i]);
+    if (!silu) return;
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+        const __half2 h = __floats2half2_rn(0.5f * v[i], 0.5f * v[i + 1]);
+        uint32_t hu = *reinterpret_cast<const uint32_t*>(&h), tu;
+        asm("tanh.approx.f16x2 %0, %1;" : "=r"(tu) : "r"(hu));
+        const float2 t = __half22float2(*reinterpret_cast<const __half2*>(&tu));
+        v[i] *= fmaf(0.5f, t.x, 0.5f);
+        v[i + 1] *= fmaf(0.5f, t.y, 0.5f);
     }
 }
 
@@ -61,34 +119,21 @@ __device__ __forceinline__ void gn_block_stats(const GnPlan& p, int img, float* 
     const int g0 = c / cg, split = (g0 + 1) * cg - c;
     const int px0 = blockIdx.x * p.px_per_block;
     const int px1 = min(p.HW, px0 + p.px_per_block);
-    float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
+    float as[8] = {}, aq[8] = {};  // per-channel sums; split into the <= 2 groups once at the end
     if (py < PY) {
         for (int base = px0 + py; base < px1; base += 8 * PY) {
-            float v[8][8];
+            uint4 raw[8];  // packed bf16: 32 registers for 8 loads in flight
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
                 const int px = base + k * PY;
-                if (px < px1) load8(gn_src(p, img, px, c), v[k]);
-                else {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) v[k][i] = 0.f;
-                }
+                raw[k] = px < px1 ? *reinterpret_cast<const uint4*>(gn_src(p, img, px, c)) : make_uint4(0, 0, 0, 0);
             }
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    if (i < split) {
-                        s0 += v[k][i];
-                        q0 += v[k][i] * v[k][i];
-                    } else {
-                        s1 += v[k][i];
-                        q1 += v[k][i] * v[k][i];
-                    }
-                }
-            }
+            for (int k = 0; k < 8; ++k) gn_acc8(raw[k], as, aq);
         }
     }
+    float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
+    gn_split8(as, aq, split, s0, q0, s1, q1);
     // fixed-order reduction: per octet over pixel lanes, then per group over octets
     float* mine = sm + (static_cast<long long>(py) * noct + ox) * 4;
     if (py < PY) {
@@ -133,13 +178,13 @@ __device__ __forceinline__ void gn_block_apply(const GnPlan& p, int img, float (
     const int c = ox * 8;
     const int px0 = blockIdx.x * p.px_per_block;
     const int px1 = min(p.HW, px0 + p.px_per_block);
-    float v[8][8];
+    uint4 raw[8];  // packed bf16
     int base = px0 + py;
     if (py < PY) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int px = base + k * PY;
-            if (px < px1) load8(gn_src(p, img, px, c), v[k]);
+            if (px < px1) raw[k] = *reinterpret_cast<const uint4*>(gn_src(p, img, px, c));
         }
     }
     for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
@@ -175,24 +220,22 @@ __device__ __forceinline__ void gn_block_apply(const GnPlan& p, int img, float (
         for (int k = 0; k < 8; ++k) {
             const int px = base + k * PY;
             if (px >= px1) continue;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float y = fmaf(v[k][i], sc[i], sh[i]);
-                v[k][i] = p.silu ? __fdividef(y, 1.f + __expf(-y)) : y;
-            }
-            store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v[k]);
+            float v[8];
+            unpack8(raw[k], v);
+            gn_affine8(v, sc, sh, p.silu);
+            store8(p.out + (static_cast<long long>(img) * p.HW + px) * Ct + c, v);
         }
         base += 8 * PY;
         if (base >= px1) break;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int px = base + k * PY;
-            if (px < px1) load8(gn_src(p, img, px, c), v[k]);
+            if (px < px1) raw[k] = *reinterpret_cast<const uint4*>(gn_src(p, img, px, c));
         }
     }
 }
 
-__global__ void __launch_bounds__(320) gn_stats_kernel(GnPlan p) {
+__global__ void __launch_bounds__(320, 3) gn_stats_kernel(GnPlan p) {
     pdl_launch();
     pdl_wait();
     const int img = blockIdx.y;
@@ -201,7 +244,7 @@ __global__ void __launch_bounds__(320) gn_stats_kernel(GnPlan p) {
     gn_block_stats(p, img, sm);
 }
 
-__global__ void __launch_bounds__(320) gn_apply_kernel(GnPlan p) {
+__global__ void __launch_bounds__(320, 3) gn_apply_kernel(GnPlan p) {
     pdl_launch();
     pdl_wait();
     const int img = blockIdx.y;
@@ -244,6 +287,198 @@ __global__ void __launch_bounds__(320) gn_fused_kernel(GnPlan p) {
     __syncthreads();
     if (!live) return;
     gn_block_apply(p, img, reinterpret_cast<float (*)[2]>(sm));
+}
+
+// One launch per GroupNorm, one thread-block cluster per image.  Each CTA owns
+// a contiguous pixel range of its image and streams it through two 100 KB
+// shared-memory buffers with bulk async copies (cp.async.bulk, mbarrier
+// completion; x1 and x2 rows are each one contiguous block), summing
+// (sum, sum of squares) per channel octet.  The block's per-group partials
+// (fixed-order fp32 reduction) are published by a cluster barrier; every CTA
+// adds the cluster's partials of each group in rank order over DSMEM in fp64,
+// so all CTAs derive bit-identical statistics.  The apply pass reads the range
+// from shared memory when it fit (<= 2 pieces) or streams it again (L2), and
+// stores y = GN(x) (+ SiLU) with 16-byte vector stores.  No statistics arena,
+// no atomics, no second launch.
+constexpr int kGnBufBytes = 100 * 1024;
+
+__device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank) {
+    uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(r) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(bytes), "r"(static_cast<uint32_t>(__cvta_generic_to_shared(bar)))
+                 : "memory");
+}
+
+__device__ __forceinline__ void gn_mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "GNW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+        "@!p bra GNW_%=;\n\t}" ::"r"(a),
+        "r"(parity)
+        : "memory");
+}
+
+__global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
+    extern __shared__ __align__(128) uint8_t gbuf[];  // [2][kGnBufBytes]
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ float sm[320 * 4];
+    __shared__ float gpart[64];  // this CTA's (sum, sum of squares) per group
+    __shared__ float st[32][2];
+    pdl_launch();
+    const int img = blockIdx.y;
+    const int Ct = p.C1 + p.C2;
+    const int noct = Ct / 8;
+    const int PY = blockDim.x / noct;
+    const int ox = threadIdx.x % noct, py = threadIdx.x / noct;
+    const int cg = Ct / p.groups;
+    const int c = ox * 8;
+    const int g0 = c / cg, split = (g0 + 1) * cg - c;
+    const int px0 = blockIdx.x * p.px_per_block;
+    const int px1 = min(p.HW, px0 + p.px_per_block);
+    const int npx = max(0, px1 - px0);
+    const int P = p.piece;
+    const int np = (npx + P - 1) / P;
+    const bool resident = np <= 2;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bar[0]))));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&bar[1]))));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    pdl_wait();
+    if (p.rows_dev && img >= *p.rows_dev) return;  // the whole cluster shares the image
+    // load sequence number L: buffer L & 1, parity (L >> 1) & 1; phase A loads the
+    // pieces as L = 0 .. np-1, a non-resident phase B again as L = np .. 2np-1
+    auto issue = [&](int L, int piece) {
+        const int a0 = px0 + piece * P;
+        const int n = min(P, px1 - a0);
+        uint8_t* dst = gbuf + (L & 1) * kGnBufBytes;
+        const uint32_t b1 = static_cast<uint32_t>(n) * p.C1 * 2, b2 = static_cast<uint32_t>(n) * p.C2 * 2;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(&bar[L & 1]))),
+                     "r"(b1 + b2)
+                     : "memory");
+        bulk_g2s(dst, p.x1 + (static_cast<long long>(img) * p.HW + a0) * p.C1, b1, &bar[L & 1]);
+        if (p.C2) bulk_g2s(dst + b1, p.x2 + (static_cast<long long>(img) * p.HW + a0) * p.C2, b2, &bar[L & 1]);
+    };
+    // this thread's octet of local pixel pl of a piece of n pixels in buffer buf,
+    // and the byte step to pixel pl + PY
+    const bool in1 = c < p.C1;
+    auto octet_ptr = [&](const uint8_t* buf, int n, int pl) -> const uint8_t* {
+        return in1 ? buf + (pl * p.C1 + c) * 2 : buf + (n * p.C1 + pl * p.C2 + (c - p.C1)) * 2;
+    };
+    auto octet_step = [&](int) -> int { return PY * (in1 ? p.C1 : p.C2) * 2; };
+    if (threadIdx.x == 0) {
+        if (np > 0) issue(0, 0);
+        if (np > 1) issue(1, 1);
+    }
+    float as[8] = {}, aq[8] = {};
+    for (int i = 0; i < np; ++i) {
+        gn_mbar_wait(&bar[i & 1], (i >> 1) & 1);
+        const uint8_t* buf = gbuf + (i & 1) * kGnBufBytes;
+        const int n = min(P, px1 - (px0 + i * P));
+        const uint8_t* q = octet_ptr(buf, n, py);
+        const int step = octet_step(n);
+        for (int pl = py; pl < n; pl += PY, q += step) gn_acc8(*reinterpret_cast<const uint4*>(q), as, aq);
+        if (!resident) {
+            __syncthreads();  // buffer consumed
+            if (threadIdx.x == 0) {
+                if (i + 2 < np) issue(i + 2, i + 2);
+                else issue(i + 2, i + 2 - np);  // phase B's first two pieces
+            }
+        }
+    }
+    float s0 = 0.f, q0 = 0.f, s1 = 0.f, q1 = 0.f;
+    gn_split8(as, aq, split, s0, q0, s1, q1);
+    float* mine = sm + (py * noct + ox) * 4;
+    mine[0] = s0;
+    mine[1] = q0;
+    mine[2] = s1;
+    mine[3] = q1;
+    __syncthreads();
+    float red[4] = {0.f, 0.f, 0.f, 0.f};
+    if (threadIdx.x < noct)
+        for (int y = 0; y < PY; ++y)
+            for (int j = 0; j < 4; ++j) red[j] += sm[(y * noct + threadIdx.x) * 4 + j];
+    __syncthreads();
+    if (threadIdx.x < noct)
+        for (int j = 0; j < 4; ++j) sm[threadIdx.x * 4 + j] = red[j];
+    __syncthreads();
+    for (int g = threadIdx.x; g < p.groups; g += blockDim.x) {
+        float a = 0.f, b = 0.f;
+        const int o0 = (g * cg) / 8, o1 = ((g + 1) * cg - 1) / 8;
+        for (int o = o0; o <= o1; ++o) {
+            const int part = (o * 8) / cg == g ? 0 : 2;
+            a += sm[o * 4 + part];
+            b += sm[o * 4 + part + 1];
+        }
+        gpart[2 * g] = a;
+        gpart[2 * g + 1] = b;
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    if (threadIdx.x < p.groups) {
+        const int g = threadIdx.x;
+        double a = 0.0, b = 0.0;
+        for (uint32_t r = 0; r < gridDim.x; ++r) {  // grid.x == cluster size
+            a += static_cast<double>(ld_dsmem_f32(&gpart[2 * g], r));
+            b += static_cast<double>(ld_dsmem_f32(&gpart[2 * g + 1], r));
+        }
+        const double n = static_cast<double>(cg) * p.HW;
+        const double m = a / n;
+        double var = b / n - m * m;
+        if (var < 0) var = 0;
+        st[g][0] = static_cast<float>(m);
+        st[g][1] = static_cast<float>(1.0 / sqrt(var + p.eps));
+    }
+    // remote reads issued: release the partials (the matching wait is at exit)
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    __syncthreads();
+    const float m0 = st[g0][0], r0 = st[g0][1];
+    const float m1 = split < 8 ? st[g0 + 1][0] : 0.f, r1 = split < 8 ? st[g0 + 1][1] : 0.f;
+    float sc[8], sh[8];
+    {
+        const float4 ga = *reinterpret_cast<const float4*>(p.gamma + c), gb = *reinterpret_cast<const float4*>(p.gamma + c + 4);
+        const float4 ba = *reinterpret_cast<const float4*>(p.beta + c), bb = *reinterpret_cast<const float4*>(p.beta + c + 4);
+        const float gam[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+        const float bet[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float m = i < split ? m0 : m1, r = i < split ? r0 : r1;
+            sc[i] = r * gam[i];
+            sh[i] = bet[i] - m * r * gam[i];
+        }
+    }
+    for (int i = 0; i < np; ++i) {
+        const int L = resident ? i : np + i;
+        if (!resident) gn_mbar_wait(&bar[L & 1], (L >> 1) & 1);
+        const uint8_t* buf = gbuf + (L & 1) * kGnBufBytes;
+        const int a0 = px0 + i * P;
+        const int n = min(P, px1 - a0);
+        const uint8_t* q = octet_ptr(buf, n, py);
+        const int step = octet_step(n);
+        bf16* o = p.out + (static_cast<long long>(img) * p.HW + a0 + py) * Ct + c;
+        for (int pl = py; pl < n; pl += PY, q += step, o += static_cast<long long>(PY) * Ct) {
+            float v[8];
+            unpack8(*reinterpret_cast<const uint4*>(q), v);
+            gn_affine8(v, sc, sh, p.silu);
+            store8(o, v);
+        }
+        if (!resident && i + 2 < np) {
+            __syncthreads();
+            if (threadIdx.x == 0) issue(L + 2, i + 2);
+        }
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // ---- LayerNorm (one warp per row) ------------------------------------------------
@@ -540,15 +775,45 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
     if (Ct % 8 != 0 || Ct % p.groups != 0 || (p.C2 && p.C1 % 8 != 0))
         raise(SDX_INVALID_ARGUMENT, "groupnorm: channels must be multiples of 8 and 32");
     if (Ct / 8 > 320) raise(SDX_INVALID_ARGUMENT, "groupnorm: more than 2560 channels");
+    // each thread owns one aligned channel octet, which must span <= 2 groups
+    if (Ct / p.groups < 8 && Ct / p.groups != 4) raise(SDX_INVALID_ARGUMENT, "groupnorm: channels per group must be 4 or >= 8");
     if (!acc) raise(SDX_INVALID_ARGUMENT, "groupnorm: statistics arena required");
-    // ~3 blocks per SM over all images, every thread >= 8 pixels
+    // one wave: as many blocks as are co-resident (occupancy of the heavier
+    // apply kernel), split evenly over the images; every thread >= 8 pixels
     const int noct = Ct / 8;
     const int PY = noct >= 256 ? 1 : 256 / noct;
-    int blocks_per_img = (3 * 148 + imgs - 1) / imgs;
+    static int resident[321] = {};  // per thread count
+    const int thr = noct * PY;
+    if (!resident[noct]) {
+        int a = 0, b = 0;
+        SDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, gn_apply_kernel, thr, 0));
+        SDX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gn_stats_kernel, thr, static_cast<size_t>(thr) * 16));
+        resident[noct] = std::max(1, std::min(a, b)) * 148;
+    }
+    int blocks_per_img = std::max(1, resident[noct] / imgs);
     int ppb = (HW + blocks_per_img - 1) / blocks_per_img;
     if (ppb < 8 * PY) ppb = 8 * PY;
     p.px_per_block = ppb;
     p.chunks = (HW + ppb - 1) / ppb;
+    // Cluster variant: one launch, one CTA cluster per image (16 CTAs up to 4 images,
+    // else 8 so the clusters are co-resident).  It uses imgs x 16|8 SMs, so it wins
+    // while each CTA's range is small (tools/gn_bench.py on B200: up to ~200 KB per
+    // CTA at <= 4 images, ~48 KB at 8); larger tensors take the statistics + apply
+    // pair over all SMs.  SDX_GN_CLUSTER_MAX (elements per image) overrides.
+    {
+        const char* cs = std::getenv("SDX_GN_CLUSTER_SIZE");
+        const int csize = cs ? std::atoi(cs) : (imgs <= 4 ? 16 : 8);
+        const long long per_cta = static_cast<long long>(HW) * Ct * 2 / std::max(1, csize);
+        bool use = per_cta <= (imgs <= 4 ? 200 * 1024 : 48 * 1024);
+        if (const char* ce = std::getenv("SDX_GN_CLUSTER_MAX")) use = static_cast<long long>(HW) * Ct <= std::atoll(ce);
+        if (use && csize >= 1 && csize <= 16) {
+            p.cluster = csize;
+            p.px_per_block = (HW + csize - 1) / csize;
+            p.chunks = csize;
+            p.piece = kGnBufBytes / (Ct * 2);
+            return p;
+        }
+    }
     // single-launch variant: grid must be co-resident -> grow the pixel range per block
     p.counter = counter;
     p.fused = 0;
@@ -580,6 +845,30 @@ void free_groupnorm(GnPlan&) {}
 void run_groupnorm(const GnPlan& p, cudaStream_t st) {
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
+    if (p.cluster) {
+        static const bool attr = [] {
+            SDX_CUDA(cudaFuncSetAttribute(gn_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            SDX_CUDA(cudaFuncSetAttribute(gn_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kGnBufBytes));
+            return true;
+        }();
+        (void)attr;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(p.cluster, p.imgs);
+        cfg.blockDim = dim3(noct * std::max(1, 320 / noct));
+        cfg.dynamicSmemBytes = 2 * kGnBufBytes;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = p.cluster;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        SDX_CUDA(cudaLaunchKernelEx(&cfg, gn_cluster_kernel, p));
+        return;
+    }
     const int PY = noct >= 256 ? 1 : 256 / noct;
     const int threads = noct * PY;
     if (p.fused && !p.stats_fused) {
@@ -591,6 +880,16 @@ void run_groupnorm(const GnPlan& p, cudaStream_t st) {
         launch_pdl(gn_stats_kernel, dim3(p.chunks, p.imgs), dim3(threads), static_cast<size_t>(threads) * 4 * sizeof(float), st, p);
     }
     launch_pdl(gn_apply_kernel, dim3(p.chunks, p.imgs), dim3(threads), 0, st, p);
+}
+
+void run_groupnorm_part(const GnPlan& p, int part, cudaStream_t st) {
+    const int noct = (p.C1 + p.C2) / 8;
+    const int PY = noct >= 256 ? 1 : 256 / noct;
+    const int threads = noct * PY;
+    if (part == 0)
+        launch_pdl(gn_stats_kernel, dim3(p.chunks, p.imgs), dim3(threads), static_cast<size_t>(threads) * 4 * sizeof(float), st, p);
+    else
+        launch_pdl(gn_apply_kernel, dim3(p.chunks, p.imgs), dim3(threads), 0, st, p);
 }
 
 void run_layernorm(const bf16* x, int rows, int C, const float* gamma, const float* beta, float eps, bf16* out,

@@ -32,11 +32,16 @@ struct GnPlan {
     int fused;
     int imgs;
     const int* rows_dev;
+    // single launch, one thread-block cluster of `cluster` CTAs per image (DSMEM
+    // statistics), pixel ranges streamed through shared memory in `piece`-pixel pieces
+    int cluster, piece;
 };
 GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
                       const float* beta, int silu, bf16* out, const int* rows_dev, unsigned long long* acc,
                       unsigned long long* counter = nullptr);
 void run_groupnorm(const GnPlan& p, cudaStream_t st);
+// one pass of the pair (0 statistics, 1 apply), for timing
+void run_groupnorm_part(const GnPlan& p, int part, cudaStream_t st);
 void free_groupnorm(GnPlan& p);
 
 // LayerNorm over the last dim C of [rows][C] (fp32 stats), bf16 out.

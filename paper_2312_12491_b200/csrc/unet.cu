@@ -77,7 +77,7 @@ GnPlan UNet::groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, f
         const char* v = std::getenv("SDX_GN_FUSE");
         return v && v[0] == '1';
     }();
-    if (enabled && fusable) {
+    if (enabled && fusable && !gp.cluster) {
         const int Ct = C1 + (x2 ? C2 : 0);
         GnSink s;
         s.acc = acc;

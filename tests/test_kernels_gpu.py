@@ -236,3 +236,33 @@ def test_conv3x3_halo(K, imgs, H, W, act, res):
     if res:
         ref = ref + R.float()
     check(out, ref)
+
+
+@pytest.mark.parametrize("cfg", [(4096, 320, 0, 4, 1), (1024, 640, 640, 2, 1), (64, 1280, 1280, 3, 0),
+                                 (256, 1920, 640, 1, 1), (4096, 128, 0, 1, 0)])
+@pytest.mark.parametrize("path", ["cluster", "split"])
+def test_groupnorm(K, cfg, path, monkeypatch):
+    """GroupNorm(32) (+ SiLU) over the channel concat [x1 | x2], NHWC bf16, against
+    torch.nn.functional.group_norm in fp32.  Paths: one launch with a 16-CTA cluster
+    per image (DSMEM statistics), or statistics (fixed-point atomics) + apply."""
+    monkeypatch.setenv("SDX_GN_CLUSTER_MAX", "0" if path == "split" else str(1 << 60))
+    HW, C1, C2, imgs, silu = cfg
+    vp = C.c_void_p
+    K.sdx_kernel_groupnorm.argtypes = [vp, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_float, vp, vp, C.c_int, vp,
+                                       vp, C.c_int, vp]
+    g = torch.Generator(device="cuda").manual_seed(HW + C1 + C2)
+    x1 = (torch.randn(imgs, HW, C1, device="cuda", generator=g) * 2 + 0.5).bfloat16()
+    x2 = (torch.randn(imgs, HW, C2, device="cuda", generator=g) - 1).bfloat16() if C2 else None
+    Ct = C1 + C2
+    gamma = torch.randn(Ct, device="cuda", generator=g)
+    beta = torch.randn(Ct, device="cuda", generator=g)
+    out = torch.empty(imgs, HW, Ct, device="cuda", dtype=torch.bfloat16)
+    arena = torch.zeros(imgs * 64 + 1, device="cuda", dtype=torch.int64)
+    st = K.sdx_kernel_groupnorm(ptr(x1), C1, ptr(x2), C2, HW, imgs, 1e-5, ptr(gamma), ptr(beta), silu, ptr(out),
+                                ptr(arena), 2, stream())
+    assert st == 0, K.sdx_kernel_last_error()
+    x = torch.cat([x1, x2], -1) if C2 else x1
+    ref = torch.nn.functional.group_norm(x.float().permute(0, 2, 1), 32, gamma, beta, 1e-5).permute(0, 2, 1)
+    if silu:
+        ref = torch.nn.functional.silu(ref)
+    check(out, ref)

@@ -66,7 +66,14 @@ def conv(imgs, H, cin, cout, stride=1):
                                              out.data_ptr(), 0, 0, 0, hp))
 
 
-conv(4, 64, 320, 320)
-conv(4, 32, 640, 640)
-gemm(16384, 320, 1280, True)
-gemm(8192, 8192, 8192)
+if len(sys.argv) > 1 and sys.argv[1] == "small":
+    # the UNet's small-K linears at 4 rows
+    gemm(16384, 320, 320, True)
+    gemm(1024, 1280, 1280, True)
+    gemm(4096, 640, 640, True)
+    gemm(1024, 1280, 1280)
+else:
+    conv(4, 64, 320, 320)
+    conv(4, 32, 640, 640)
+    gemm(16384, 320, 1280, True)
+    gemm(8192, 8192, 8192)
