@@ -29,7 +29,12 @@ namespace {
 
 constexpr int BQ = 128, BKV = 128, HD = 64;
 constexpr uint32_t TILE_BYTES = 128 * 64 * 2;  // one 128-row x 64-col bf16 tile (16 KB)
-constexpr int KVS = 4;  // K/V ring depth: TMA latency (~1-2 us under load) exceeds one block's compute
+// P buffers per q tile: with 2, the softmax of block j+1 writes P while PV(j) still
+// reads the other buffer (it waits only for PV(j-1)), but the K/V ring must shrink to
+// 2 to fit in shared memory; measured on B200 (tools/attn_probe.py, 4 x 4096 x 5
+// heads): PB=2/KVS=2 210.7 us vs PB=1/KVS=4 190.2 us, so one buffer.
+constexpr int PB = 1;
+constexpr int KVS = PB == 2 ? 2 : 4;  // K/V ring depth
 
 __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
     const uint32_t a = smem_u32(bar);
@@ -109,15 +114,15 @@ __global__ void __launch_bounds__(320, 1)
     uint8_t* sQ = smem;                       // 2 x 16 KB
     uint8_t* sK = sQ + 2 * TILE_BYTES;        // KVS x 16 KB
     uint8_t* sV = sK + KVS * TILE_BYTES;      // KVS x 16 KB
-    uint8_t* sP = sV + KVS * TILE_BYTES;      // 2 tiles x 32 KB (two 64-key atoms each)
-    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * TILE_BYTES);
+    uint8_t* sP = sV + KVS * TILE_BYTES;      // [2 tiles][PB] x 32 KB (two 64-key atoms each)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sP + 4 * PB * TILE_BYTES);
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;          // [KVS]
     uint64_t* kv_empty = kv_full + KVS;    // [KVS]
     uint64_t* s_full = kv_empty + KVS;     // [2] per tile
-    uint64_t* p_full = s_full + 2;         // [2] per tile
-    uint64_t* pv_done = p_full + 2;        // [2] per tile
-    uint64_t* s_free = pv_done + 2;        // [2] per tile: S read out of TMEM (next S may overwrite it)
+    uint64_t* p_full = s_full + 2;         // [2 tiles][PB]: P buffer written
+    uint64_t* pv_done = p_full + 2 * PB;   // [2 tiles][PB]: PV that read the P buffer done
+    uint64_t* s_free = pv_done + 2 * PB;   // [2] per tile: S read out of TMEM (next S may overwrite it)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -136,9 +141,11 @@ __global__ void __launch_bounds__(320, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
+            mbar_init(&s_free[i], 4);  // one arrival per softmax warp
+        }
+        for (int i = 0; i < 2 * PB; ++i) {
             mbar_init(&p_full[i], 128);
             mbar_init(&pv_done[i], 1);
-            mbar_init(&s_free[i], 4);  // one arrival per softmax warp
         }
         fence_barrier_init();
     }
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(320, 1)
                 umma_commit(&s_full[t]);
             };
             auto issue_pv = [&](int t, int j) {
-                const uint32_t pbase = smem_u32(sP + t * 2 * TILE_BYTES);
+                const uint32_t pbase = smem_u32(sP + (t * PB + j % PB) * 2 * TILE_BYTES);
                 const uint32_t vbase = smem_u32(sV + (j % KVS) * TILE_BYTES);
 #pragma unroll
                 for (int k = 0; k < ((a.xmode == 1 || a.xmode == 5 || a.xmode == 7) ? 0 : BKV / 16); ++k) {
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(320, 1)
                     const uint64_t dv = desc_mnmajor_sw128(vbase + k * 2048, 0);
                     umma_f16(tmem + t * 192 + 128, dp, dv, idesc_o, (j > 0 || k != 0) ? 1u : 0u);
                 }
-                umma_commit(&pv_done[t]);
+                umma_commit(&pv_done[t * PB + j % PB]);
             };
             wait_bar(&kv_full[0], 0);
             tc_fence_after();
@@ -213,7 +220,7 @@ __global__ void __launch_bounds__(320, 1)
                         ++ns[t];
                         progress = true;
                     }
-                    if (np[t] < ns[t] && mbar_test(&p_full[t], np[t] & 1)) {
+                    if (np[t] < ns[t] && mbar_test(&p_full[t * PB + np[t] % PB], (np[t] / PB) & 1)) {
                         tc_fence_after();
                         issue_pv(t, np[t]);
                         ++np[t];
@@ -239,8 +246,8 @@ __global__ void __launch_bounds__(320, 1)
             const uint32_t o_addr = s_addr + 128;
             const float sl2 = a.scale * 1.4426950408889634f;
             float m_used = -INFINITY, l = 0.f;
-            uint8_t* prow = sP + t * 2 * TILE_BYTES;
             for (int j = 0; j < nkv; ++j) {
+                uint8_t* prow = sP + (t * PB + j % PB) * 2 * TILE_BYTES;
                 wait_bar(&s_full[t], j & 1);
                 tc_fence_after();
                 uint32_t sr[128];
@@ -276,12 +283,15 @@ __global__ void __launch_bounds__(320, 1)
                 const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                        fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
                 const float m_row = mx * sl2;
-                if (j > 0) wait_bar(&pv_done[t], (j - 1) & 1);  // PV(j-1) finished reading P_t and writing O_t
+                // PV(j - PB) finished reading this P buffer
+                if (j >= PB) wait_bar(&pv_done[t * PB + j % PB], ((j - PB) / PB) & 1);
                 if (m_row > m_used + 8.f) {
                     // lazy rescale: new reference max for this row
                     const float m_new = m_row;
                     const float corr = ex2(m_used - m_new);  // m_used = -inf -> 0
                     if (j > 0) {
+                        // O_t is final through block j-1 once PV(j-1) is done
+                        if (PB > 1) wait_bar(&pv_done[t * PB + (j - 1) % PB], ((j - 1) / PB) & 1);
                         tc_fence_after();
 #pragma unroll
                         for (int c = 0; c < HD; c += 16) {
@@ -316,9 +326,9 @@ __global__ void __launch_bounds__(320, 1)
                 l += ((sum8[0] + sum8[1]) + (sum8[2] + sum8[3])) + ((sum8[4] + sum8[5]) + (sum8[6] + sum8[7]));
                 fence_async_smem();
                 tc_fence_before();
-                mbar_arrive(&p_full[t]);
+                mbar_arrive(&p_full[t * PB + j % PB]);
             }
-            wait_bar(&pv_done[t], (nkv - 1) & 1);
+            wait_bar(&pv_done[t * PB + (nkv - 1) % PB], ((nkv - 1) / PB) & 1);
             tc_fence_after();
             const int qi = q_first + t * BQ + r;
             float o[HD];
@@ -407,7 +417,7 @@ void set_attention_probe_mode(int mode) { g_attn_xmode = mode; }
 
 void run_attention(const AttnPlan& p, cudaStream_t st) {
     static bool attr = false;
-    const size_t smem = (2 + 2 * KVS + 4) * TILE_BYTES + 1024 + 256;
+    const size_t smem = (2 + 2 * KVS + 4 * PB) * TILE_BYTES + 1024 + 256;
     if (!attr) {
         SDX_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         attr = true;

@@ -12,6 +12,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -1144,6 +1145,16 @@ void set_gemm_tiling_override(int bn, int splits, int pair) {
 //   per CTA              ceil(units / slots) x max(mainloop, epilogue) + pipeline fill + last epilogue
 //   split-K              + fp32 partial traffic and the reduce kernel
 double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual, bool pair) {
+    // Constants fitted (tools/fit_tiling.py) to a graph-timed sweep of every (BN, split-K,
+    // pair) candidate on the UNet's GEMM / conv shapes at 2, 4 and 8 rows on B200
+    // (tools/gemm_sweep.py, SDX_SWEEP_JSON): the objective is the summed measured time of
+    // the candidate the model picks, 1.6% above the per-shape optimum.  Cycles:
+    //   slice  = one 64-deep K slice through the MMA pipe (floor ~ the per-instruction cost
+    //            of tcgen05.mma, which barely grows with N up to 224)
+    //   epi    = one tile's epilogue + tile hand-off; both overlap across tiles
+    //   split  = fp32 partial traffic and the reduce kernel; pair = cluster overheads
+    constexpr double a0 = 411.0, a1 = 1.06, a2 = 1.66, a3 = 31.7;
+    constexpr double e0 = 0.016, e1 = 13300.0, c0 = 8830.0, p0 = 10800.0, s0 = 2520.0, s1 = 14.4;
     const long long mu = pair ? 256 : 128;
     const long long slots = pair ? kSmCount / 2 : kSmCount;
     const long long mt = (M + mu - 1) / mu, nt = (N + bn - 1) / bn;
@@ -1151,15 +1162,16 @@ double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, b
     const int nk = K / 64;
     const double bnl = pair ? bn / 2.0 : bn;
     const double nku = static_cast<double>((nk + splits - 1) / splits);
-    const double slice = (2.0 * bn > 2.0 * (128.0 + bnl) ? 2.0 * bn : 2.0 * (128.0 + bnl)) + 40.0;
+    const double slice = std::max({a0, a1 * bn, a2 * (128.0 + bnl)}) + a3;
     const double ml = nku * slice;
     const double eb = splits > 1 ? 4.0 : out_bytes + (residual ? 2.0 : 0.0);
-    const double epi = 128.0 * bn * eb / 16.0 + 400.0;
+    const double epi = e0 * 128.0 * bn * eb / 16.0 + e1;
     const double per_cta = static_cast<double>((units + slots - 1) / slots);
-    double t = per_cta * (ml > epi ? ml : epi) + 1500.0 + (ml < epi ? ml : epi);
+    double t = per_cta * std::max(ml, epi) + c0 + std::min(ml, epi);
+    if (pair) t += p0;
     if (splits > 1) {
         const double bytes = static_cast<double>(M) * N * (4.0 * splits + out_bytes + (residual ? 2.0 : 0.0));
-        t += 5000.0 + bytes / (kSmCount * 16.0);
+        t += s0 + bytes / (kSmCount * s1);
     }
     return t;
 }

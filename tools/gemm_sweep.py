@@ -5,6 +5,8 @@ replays of a prebuilt plan, next to the cost model's pick.
     python tools/gemm_sweep.py [rows ...]
 """
 import ctypes as C
+import json
+import os
 import sys
 
 import torch
@@ -55,13 +57,17 @@ def info(h):
     return bn.value, s.value, clk.value
 
 
-def sweep(label, make, flops, N, K):
+RECORDS = []  # every timed candidate, for fitting the tiling cost model (SDX_SWEEP_JSON)
+
+
+def sweep(label, make, flops, N, K, M=0, res=False):
     h = vp()
     assert make(0, 0, C.byref(h)) == 0, L.sdx_kernel_last_error()
     mbn, ms, mclk = info(h)
     tm = time_plan(h)
     L.sdx_kernel_plan_destroy(h)
     best = (tm, mbn, ms)
+    RECORDS.append({"label": label, "M": M, "N": N, "K": K, "res": res, "bn": mbn, "s": ms, "us": tm, "model": True})
     for bn in BNS:
         if N <= 64 and abs(bn) > 64:
             continue
@@ -75,6 +81,8 @@ def sweep(label, make, flops, N, K):
                 continue
             t = time_plan(h)
             L.sdx_kernel_plan_destroy(h)
+            RECORDS.append({"label": label, "M": M, "N": N, "K": K, "res": res, "bn": bn, "s": s, "us": t,
+                            "model": False})
             if t < best[0]:
                 best = (t, bn, s)
     print(f"{label:44s} model bn={mbn:3d} s={ms:2d} {tm:7.1f} us ({flops / tm / 1e6:6.1f} TF/s, model {mclk / 1965:6.1f} us)"
@@ -94,7 +102,7 @@ def gemm_case(M, N, K, res):
         return L.sdx_kernel_gemm_plan(A.data_ptr(), K, B.data_ptr(), K, out.data_ptr(), M, N, K, bias.data_ptr(),
                                       R.data_ptr() if res else None, 0, 0, bn, s, hp)
 
-    return sweep(f"linear M={M} N={N} K={K}{' +res' if res else ''}", make, 2.0 * M * N * K, N, K)
+    return sweep(f"linear M={M} N={N} K={K}{' +res' if res else ''}", make, 2.0 * M * N * K, N, K, M, res)
 
 
 def conv_case(imgs, H, Cin, Cout, stride=1):
@@ -109,7 +117,7 @@ def conv_case(imgs, H, Cin, Cout, stride=1):
                                          None, 0, out.data_ptr(), 0, bn, s, hp)
 
     return sweep(f"conv3x3 {imgs}x{H}^2 {Cin}->{Cout} s{stride}", make, 2.0 * imgs * Ho * Ho * Cout * 9 * Cin, Cout,
-                 9 * Cin)
+                 9 * Cin, imgs * Ho * Ho, False)
 
 
 def main():
@@ -139,6 +147,8 @@ def main():
                               (256, 64, 64, 2), (128, 64, 64, 2)):
         a, b = conv_case(1, H, cin, cout, s)
     print(f"sum over UNet shapes: model {tot_m:.1f} us, best {tot_b:.1f} us")
+    if os.environ.get("SDX_SWEEP_JSON"):
+        json.dump(RECORDS, open(os.environ["SDX_SWEEP_JSON"], "w"))
 
 
 if __name__ == "__main__":
