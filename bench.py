@@ -371,6 +371,9 @@ def cpu_reference(args, seconds: float, steps: int = 1, warmup: int = 0):
 
 def main():
     args = parse()
+    if os.environ.get("SDX_ABLATE"):
+        # op-skipping timing ablation (unet.cu): never a bench number
+        sys.exit("bench.py: SDX_ABLATE is set (skips UNet ops); unset it to measure")
     if args.impl == "reference":
         rank = int(os.environ.get("RANK", "0"))
         if rank != 0:

@@ -35,6 +35,11 @@ constexpr uint32_t TILE_BYTES = 128 * 64 * 2;  // one 128-row x 64-col bf16 tile
 // heads): PB=2/KVS=2 210.7 us vs PB=1/KVS=4 190.2 us, so one buffer.
 constexpr int PB = 1;
 constexpr int KVS = PB == 2 ? 2 : 4;  // K/V ring depth
+// How far QK^T may run ahead of PV per tile (S_t(j+1) also needs s_free: S_t(j) read
+// into registers).  2 lets S(j+1) overlap the softmax of block j; measured equal to 1
+// (190.7 vs 190.2 us, tools/attn_probe.py): the softmax warps, not the MMA order, set
+// the pace.
+constexpr int kSAhead = 1;
 
 __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
     const uint32_t a = smem_u32(bar);
@@ -213,7 +218,7 @@ __global__ void __launch_bounds__(320, 1)
                 bool progress = false;
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
-                    if (ns[t] < nkv && ns[t] - np[t] <= 1 && mbar_test(&kv_full[ns[t] % KVS], (ns[t] / KVS) & 1) &&
+                    if (ns[t] < nkv && ns[t] - np[t] <= kSAhead && mbar_test(&kv_full[ns[t] % KVS], (ns[t] / KVS) & 1) &&
                         mbar_test(&s_free[t], (ns[t] - 1) & 1)) {
                         tc_fence_after();
                         issue_s(t, ns[t]);

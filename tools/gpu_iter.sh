@@ -1,7 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/t_all.txt 2>&1
-echo "tests rc=$?" >> gpurun_out/t_all.txt
-timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 > gpurun_out/b1.json 2> gpurun_out/b1.err
-timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 --streams 8 --n-steps 1 --guidance self_negative > gpurun_out/b4.json 2>> gpurun_out/b1.err
-SDX_SWEEP_JSON=gpurun_out/sweep_fit.json timeout 2400 python tools/gemm_sweep.py 2 4 8 > gpurun_out/gemm_sweep_fit.txt 2>&1
+M="--clock-control none --cache-control none"
+timeout 300 python tools/attn_probe.py > gpurun_out/attn_probe.txt 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum $M --profile-from-start off --csv --log-file gpurun_out/unet_traffic_r8.csv python tools/prof_unet.py 8 3 > gpurun_out/ncu_traffic_r8.log 2>&1
+python tools/ncu_traffic.py gpurun_out/unet_traffic_r8.csv gpurun_out/unet_traffic_r8.json "UNet forward, 8 rows (cfg4 denoiser launch)" 8 > gpurun_out/unet_traffic_r8.txt

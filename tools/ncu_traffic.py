@@ -33,6 +33,10 @@ tot_w = sum(v[3] for v in agg.values())
 print(f"{len(K)} launches, {tot_us:.1f} us (serialised, ncu), DRAM read {tot_r / 1e6:.1f} MB, write {tot_w / 1e6:.1f} MB")
 for name, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     print(f"{v[1]:9.1f} us {v[0]:4d}x  r {v[2] / 1e6:8.1f} MB  w {v[3] / 1e6:8.1f} MB  {name}")
-json.dump({"label": sys.argv[3] if len(sys.argv) > 3 else "", "launches": len(K), "ncu_serial_us": tot_us,
-           "dram_bytes_read": tot_r, "dram_bytes_write": tot_w, "dram_bytes": tot_r + tot_w},
-          open(sys.argv[2], "w"), indent=1)
+out = {"label": sys.argv[3] if len(sys.argv) > 3 else "", "launches": len(K), "ncu_serial_us": tot_us,
+       "dram_bytes_read": tot_r, "dram_bytes_write": tot_w, "dram_bytes": tot_r + tot_w}
+if len(sys.argv) > 4:  # UNet rows of the captured forward (bench.py matches its roofline traffic on it)
+    out["rows"] = int(sys.argv[4])
+    out["source"] = (f"ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum --cache-control none over one UNet "
+                     f"forward (tools/prof_unet.py {out['rows']} 3, last forward), tools/gpu_profile_round.sh")
+json.dump(out, open(sys.argv[2], "w"), indent=1)
