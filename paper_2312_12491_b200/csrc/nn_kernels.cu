@@ -791,8 +791,9 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
         resident[noct] = std::max(1, std::min(a, b)) * 148;
     }
     int blocks_per_img = std::max(1, resident[noct] / imgs);
+    // whole batches of 8 pixels per thread: a partial second batch costs a full load round trip
     int ppb = (HW + blocks_per_img - 1) / blocks_per_img;
-    if (ppb < 8 * PY) ppb = 8 * PY;
+    ppb = (ppb + 8 * PY - 1) / (8 * PY) * (8 * PY);
     p.px_per_block = ppb;
     p.chunks = (HW + ppb - 1) / ppb;
     // Cluster variant: one launch, one CTA cluster per image (16 CTAs up to 4 images,
