@@ -86,6 +86,26 @@ __global__ void unet_prep_kernel(const StreamCtl* __restrict__ ctl, const RowDes
 
 }  // namespace
 
+namespace {
+// Latents of the ingesting streams out of the per-frame encoder staging
+// (encoded ahead of the iteration): x0[enc_dst[i]] = staged[enc_src[i]].
+__global__ void enc_gather_kernel(CodecLists L, const float* __restrict__ staged, float* __restrict__ x0, long long d) {
+    const int i = blockIdx.y;
+    if (i >= *L.n_ingest) return;
+    const float4* src = reinterpret_cast<const float4*>(staged + static_cast<long long>(L.enc_src[i]) * d);
+    float4* dst = reinterpret_cast<float4*>(x0 + static_cast<long long>(L.enc_dst[i]) * d);
+    for (long long j = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; j < d / 4;
+         j += static_cast<long long>(gridDim.x) * blockDim.x)
+        dst[j] = src[j];
+}
+
+}  // namespace
+
+void launch_enc_gather(const CodecLists& L, int S, const float* staged, float* x0, long long d, cudaStream_t st) {
+    enc_gather_kernel<<<dim3(8, S), 256, 0, st>>>(L, staged, x0, d);
+    SDX_LAUNCH_CHECK();
+}
+
 void launch_ctl_lists(const StreamCtl* ctl, int S, int n, int ring_slot, const RowDesc* rows, const int* n_rows,
                       const CodecLists& L, cudaStream_t st) {
     int threads = 32;

@@ -18,6 +18,9 @@ struct CodecLists {
     int* row_prompt;  // UNet [rmax]
 };
 
+// x0[enc_dst[i]] = staged[enc_src[i]] for the n_ingest encoded frames (staged latents
+// indexed like enc_src: ring_slot * S + stream)
+void launch_enc_gather(const CodecLists& L, int S, const float* staged, float* x0, long long d, cudaStream_t st);
 void launch_ctl_lists(const StreamCtl* ctl, int S, int n, int ring_slot, const RowDesc* rows, const int* n_rows,
                       const CodecLists& L, cudaStream_t st);
 void launch_unet_prep(const StreamCtl* ctl, const RowDesc* rows, const int* n_rows, int rmax, int n, long long d,

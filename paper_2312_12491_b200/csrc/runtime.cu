@@ -509,10 +509,28 @@ Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const 
         TaesdIO io;
         io.frames = d_in_;
         io.frame_stride = pad_;
-        io.enc_src = lists_.enc_src;
-        io.enc_count = lists_.n_ingest;
-        io.latent_out = dev_.x0;
-        io.enc_dst = lists_.enc_dst;
+        // the encoder always encodes all S frames of a ring slot into enc_stage_ (identity
+        // lists of that slot, copied into enc_lists_ first); the iteration gathers
+        const int nl2 = 2 * S_ + 1;
+        enc_stage_ = dev_alloc<float>(static_cast<size_t>(K_) * S_ * d);
+        enc_lists_ = dev_alloc<int>(static_cast<size_t>(nl2));
+        spec_lists_ = dev_alloc<int>(static_cast<size_t>(K_) * nl2);
+        {
+            std::vector<int> hl(static_cast<size_t>(K_) * nl2);
+            for (int k = 0; k < K_; ++k) {
+                for (int s2 = 0; s2 < S_; ++s2) {
+                    hl[static_cast<size_t>(k) * nl2 + s2] = k * S_ + s2;       // src frame
+                    hl[static_cast<size_t>(k) * nl2 + S_ + s2] = k * S_ + s2;  // dst staging block
+                }
+                hl[static_cast<size_t>(k) * nl2 + 2 * S_] = S_;
+            }
+            SDX_CUDA(cudaMemcpy(spec_lists_, hl.data(), sizeof(int) * hl.size(), cudaMemcpyHostToDevice));
+            SDX_CUDA(cudaMemcpy(enc_lists_, hl.data(), sizeof(int) * nl2, cudaMemcpyHostToDevice));
+        }
+        io.enc_src = enc_lists_;
+        io.enc_count = enc_lists_ + 2 * S_;
+        io.latent_out = enc_stage_;
+        io.enc_dst = enc_lists_ + S_;
         // the decoder reads its own copy of the emitted latents and codec lists
         // (staged per ring slot by the main part of the iteration)
         const int nl = 4 * S_ + 2;
@@ -529,13 +547,20 @@ Pipeline::Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const 
         io.dec_dst = dec_lists_ + 3 * S_;
         const char* ov = std::getenv("SDX_DECODE_OVERLAP");
         overlap_ = !(ov && ov[0] == '0');
-        io.separate_decoder_buffers = overlap_;
+        const char* oe = std::getenv("SDX_ENCODE_OVERLAP");
+        enc_overlap_ = !(oe && oe[0] == '0');
+        io.separate_decoder_buffers = overlap_ || enc_overlap_;
         taesd_ = std::make_unique<TAESD>(S_, e.seed ^ 0x7AE5DULL, io, stream_);
         if (overlap_) {
             SDX_CUDA(cudaStreamCreateWithFlags(&dec_stream_, cudaStreamNonBlocking));
             main_done_.resize(static_cast<size_t>(K_));
             for (auto& ev : main_done_) SDX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
             SDX_CUDA(cudaEventCreateWithFlags(&dec_join_, cudaEventDisableTiming));
+        }
+        if (enc_overlap_) {
+            SDX_CUDA(cudaStreamCreateWithFlags(&enc_stream_, cudaStreamNonBlocking));
+            enc_done_.resize(static_cast<size_t>(K_));
+            for (auto& ev : enc_done_) SDX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         }
     }
     SDX_CUDA(cudaMallocHost(&h_in_, static_cast<size_t>(K_) * S_ * D_));
@@ -558,7 +583,10 @@ Pipeline::~Pipeline() {
     if (stream_) cudaStreamSynchronize(stream_);
     if (copy_) cudaStreamSynchronize(copy_);
     if (dec_stream_) cudaStreamSynchronize(dec_stream_);
+    if (enc_stream_) cudaStreamSynchronize(enc_stream_);
     for (auto gexec : graphs_)
+        if (gexec) cudaGraphExecDestroy(gexec);
+    for (auto gexec : enc_graphs_)
         if (gexec) cudaGraphExecDestroy(gexec);
     for (auto gexec : dec_graphs_)
         if (gexec) cudaGraphExecDestroy(gexec);
@@ -573,6 +601,11 @@ Pipeline::~Pipeline() {
     for (auto ev : main_done_) cudaEventDestroy(ev);
     if (dec_join_) cudaEventDestroy(dec_join_);
     if (dec_stream_) cudaStreamDestroy(dec_stream_);
+    dev_free(enc_stage_);
+    dev_free(enc_lists_);
+    dev_free(spec_lists_);
+    for (auto ev : enc_done_) cudaEventDestroy(ev);
+    if (enc_stream_) cudaStreamDestroy(enc_stream_);
     dev_.release();
     dev_free(d_in_);
     dev_free(d_ref_);
@@ -641,8 +674,9 @@ void Pipeline::launch_iteration(int k, bool frame_present) {
     }
     mark(2);
     if (taesd && frame_present) {
-        taesd_->encode(stream_);
-        launches_ += taesd_->launches_per_encode();
+        if (!(enc_overlap_ && !profile_)) launch_encode(k, stream_);  // else encoded ahead (run_encode)
+        launch_enc_gather(lists_, S_, enc_stage_, dev_.x0, d_, stream_);
+        launches_ += 1;
     }
     mark(3);
     StepArgs sa = dev_.step_args();
@@ -692,8 +726,44 @@ void Pipeline::launch_decode(int k, cudaStream_t s) {
                                  cudaMemcpyDeviceToHost, s));
 }
 
+// Encode all S frames of ring slot k into enc_stage_ (its identity lists first).
+void Pipeline::launch_encode(int k, cudaStream_t s) {
+    const int nl2 = 2 * S_ + 1;
+    SDX_CUDA(cudaMemcpyAsync(enc_lists_, spec_lists_ + static_cast<size_t>(k) * nl2, sizeof(int) * nl2,
+                             cudaMemcpyDeviceToDevice, s));
+    taesd_->encode(s);
+    launches_ += taesd_->launches_per_encode();
+}
+
+// Encode ahead: slot k's frames on enc_stream_ once they are in HBM (h2d_[k]),
+// overlapping the iterations still running; the iteration waits enc_done_[k].
+void Pipeline::run_encode(int k) {
+    SDX_CUDA(cudaStreamWaitEvent(enc_stream_, h2d_[static_cast<size_t>(k)], 0));
+    if (!cfg_.graph) {
+        launch_encode(k, enc_stream_);
+    } else {
+        if (enc_graphs_.size() < static_cast<size_t>(K_)) enc_graphs_.assign(static_cast<size_t>(K_), nullptr);
+        if (!enc_graphs_[static_cast<size_t>(k)]) {
+            const long long before = launches_;
+            cudaGraph_t g = nullptr;
+            SDX_CUDA(cudaStreamBeginCapture(enc_stream_, cudaStreamCaptureModeThreadLocal));
+            launch_encode(k, enc_stream_);
+            SDX_CUDA(cudaStreamEndCapture(enc_stream_, &g));
+            SDX_CUDA(cudaGraphInstantiate(&enc_graphs_[static_cast<size_t>(k)], g, 0));
+            SDX_CUDA(cudaGraphDestroy(g));
+            enc_graph_launches_ = launches_ - before;
+            launches_ = before;
+        }
+        SDX_CUDA(cudaGraphLaunch(enc_graphs_[static_cast<size_t>(k)], enc_stream_));
+        launches_ += enc_graph_launches_;
+    }
+    SDX_CUDA(cudaEventRecord(enc_done_[static_cast<size_t>(k)], enc_stream_));
+}
+
 // Make stream_ wait for every decode issued so far (timer marks, sync).
 void Pipeline::join_decode() {
+    // the encode-ahead stream never runs past the main stream's waits, so joining the
+    // decode stream (which waits for the main stream) covers it as well
     if (!dec_stream_) return;
     SDX_CUDA(cudaEventRecord(dec_join_, dec_stream_));
     SDX_CUDA(cudaStreamWaitEvent(stream_, dec_join_, 0));
@@ -703,6 +773,10 @@ void Pipeline::join_decode() {
 // (replaying its CUDA graph when graphs are enabled), mark completion.
 void Pipeline::run_iteration(int k, bool frame_present) {
     if (frame_present) SDX_CUDA(cudaStreamWaitEvent(stream_, h2d_[static_cast<size_t>(k)], 0));
+    if (frame_present && taesd_ && enc_overlap_ && !profile_) {
+        run_encode(k);
+        SDX_CUDA(cudaStreamWaitEvent(stream_, enc_done_[static_cast<size_t>(k)], 0));
+    }
     const bool use_graph = cfg_.graph && frame_present && !profile_;
     if (!use_graph) {
         launch_iteration(k, frame_present);

@@ -187,6 +187,8 @@ class Pipeline {
     };
     void launch_iteration(int k, bool frame_present);
     void launch_decode(int k, cudaStream_t s);
+    void launch_encode(int k, cudaStream_t s);
+    void run_encode(int k);
     void run_iteration(int k, bool frame_present);
     void join_decode();
     void process(int k, bool frame_present);
@@ -245,6 +247,18 @@ class Pipeline {
     int* dec_lists_ = nullptr;     // [4S+2]
     std::vector<cudaGraphExec_t> dec_graphs_;  // [ring slot][output-copy variant]
     std::vector<long long> dec_graph_launches_;
+    // Encode ahead (TAESD codec): the frames of ring slot k are encoded on enc_stream_
+    // as soon as they are in HBM, all S of them, into enc_stage_ (indexed like the
+    // ring, slot * S + stream) while the previous iterations run; the iteration then
+    // only gathers its ingesting streams' latents into x0 (it waits enc_done_[k]).
+    bool enc_overlap_ = false;
+    cudaStream_t enc_stream_ = nullptr;
+    std::vector<cudaEvent_t> enc_done_;  // [K]
+    float* enc_stage_ = nullptr;          // [K*S][d]
+    int* enc_lists_ = nullptr;            // [2S+1] encoder's src / dst / count
+    int* spec_lists_ = nullptr;           // [K][2S+1] per-slot identity lists
+    std::vector<cudaGraphExec_t> enc_graphs_;  // [ring slot]
+    long long enc_graph_launches_ = 0;
 };
 
 }  // namespace sdx
