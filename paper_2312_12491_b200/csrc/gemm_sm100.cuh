@@ -49,6 +49,7 @@ struct GemmEpilogue {
     int out_f32 = 0;                      // 0 bf16, 1 fp32, 2 u8 (round(255 * clamp(v, 0, 1))), 3 fp16
     int act_after_residual = 0;           // act(acc + bias + residual) instead of act(acc + bias) + residual
     int geglu = 0;                        // B rows interleaved [16 value | 16 gate]: out[:, j] = a_j * gelu(g_j), N/2 cols
+    int gelu_tanh = 0;                    // GEGLU gate as tanh-form GELU with tanh.approx (else erf GELU)
     const int* out_img_map = nullptr;     // image -> destination image block of rows_per_img rows (scatter)
     GnSink gn[2];                         // GroupNorm statistics of this output (up to two consumers)
     int n_gn = 0;

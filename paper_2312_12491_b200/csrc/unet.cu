@@ -325,6 +325,11 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
         run_interleave_geglu(w1, b1, 4 * C, C, w1i, b1i, nullptr);
         GemmEpilogue e;
         e.geglu = 1;
+        // tanh-form GELU (measured 0.64 -> 0.54 ms of GEGLU per 4-row forward); SDX_GELU_TANH=0: erf
+        e.gelu_tanh = [] {
+            const char* v = std::getenv("SDX_GELU_TANH");
+            return v && v[0] == '0' ? 0 : 1;
+        }();
         e.out = u;
         e.ld_out = 4 * C;
         ln_gemm("linear_geglu", h3, l3g, l3b, w1i, 8 * C, b1i, e);

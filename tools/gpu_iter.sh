@@ -2,6 +2,4 @@ cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/t_all.txt 2>&1
 timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 > gpurun_out/b1.json 2> gpurun_out/b1.err
-SDX_ENCODE_OVERLAP=0 timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 > gpurun_out/b1_noenc.json 2>> gpurun_out/b1.err
 timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 --streams 8 --n-steps 1 --guidance self_negative > gpurun_out/b4.json 2>> gpurun_out/b1.err
-SDX_ENCODE_OVERLAP=0 timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 --streams 8 --n-steps 1 --guidance self_negative > gpurun_out/b4_noenc.json 2>> gpurun_out/b1.err
