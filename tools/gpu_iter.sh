@@ -1,5 +1,8 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/t_all.txt 2>&1
-timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 > gpurun_out/b1.json 2> gpurun_out/b1.err
-timeout 300 python bench.py --no-cpu-baseline --steps 40 --warmup 5 --streams 8 --n-steps 1 --guidance self_negative > gpurun_out/b4.json 2>> gpurun_out/b1.err
+rm -f gpurun_out/attn_poly.txt
+for P in 0 2 3 4; do
+  echo "POLY=$P" >> gpurun_out/attn_poly.txt
+  SDX_ATTN_POLY=$P timeout 300 python tools/attn_probe.py 2>&1 | cut -c1-80 >> gpurun_out/attn_poly.txt
+done
+SDX_ATTN_POLY=4 timeout 600 python -m pytest tests/test_kernels_gpu.py tests/test_unet_gpu.py -m gpu -x -q -k "attention or unet" > gpurun_out/t_poly.txt 2>&1
