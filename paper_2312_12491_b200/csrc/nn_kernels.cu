@@ -691,6 +691,91 @@ __global__ void __launch_bounds__(256) conv3x3_rgb8_kernel(const uint8_t* __rest
     }
 }
 
+// ---- 3x3 conv, 64 -> CO (<= 4) channels, u8 output (TAESD decoder head) ----------------
+// On tensor cores this head pads N to 64 and takes twice a full 64 -> 64 conv (56 vs
+// 31 us per 512^2 image); here it is CUDA-core fp32.  Block = 4 output rows x 128
+// columns; the 6 x 130 x 64 bf16 input tile sits in smem with the 16-byte chunks
+// of each pixel XOR-swizzled by (column % 8), so 32 lanes reading consecutive
+// pixels hit distinct banks; each thread owns 4 pixels (x = p*32 + lane) of its row.
+// Weights as fp32 float4 per (tap, channel) (broadcast reads).  Two blocks per SM
+// overlap one block's tile load with the other's math.
+// fp32 accumulation, then round(255 * clamp(v, 0, 1)) like the GEMM u8 epilogue.
+constexpr int kHeadRows = 4;
+constexpr int kHeadTileBytes = (kHeadRows + 2) * 130 * 128;
+
+template <int CO>
+__global__ void __launch_bounds__(32 * kHeadRows) conv3x3_c64_u8_kernel(const bf16* __restrict__ in, int H, int W,
+                                                            const bf16* __restrict__ w, const float* __restrict__ bias,
+                                                            uint8_t* __restrict__ out, const int* img_map,
+                                                            const int* rows_dev) {
+    extern __shared__ __align__(16) uint8_t tile[];  // [rows + 2][130][8 chunks x 16 B], swizzled
+    __shared__ __align__(16) float4 ws[9][64];       // (w_o0, w_o1, w_o2, 0) per tap and channel
+    static_assert(CO <= 4, "head conv: <= 4 output channels");
+    pdl_launch();
+    pdl_wait();
+    const int n = blockIdx.z;
+    if (rows_dev && n >= *rows_dev) return;
+    const int y0 = blockIdx.y * kHeadRows, x0 = blockIdx.x * 128;
+    for (int i = threadIdx.x; i < 9 * 64; i += blockDim.x) {
+        const int c = i % 64, t = i / 64;
+        float q[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int o = 0; o < CO; ++o) q[o] = __bfloat162float(w[(static_cast<long long>(o) * 9 + t) * 64 + c]);
+        ws[t][c] = make_float4(q[0], q[1], q[2], q[3]);
+    }
+    const bf16* base = in + static_cast<long long>(n) * H * W * 64;
+    for (int i = threadIdx.x; i < (kHeadRows + 2) * 130 * 8; i += blockDim.x) {
+        const int k = i & 7, col = (i >> 3) % 130, r = i / (130 * 8);
+        const int yy = y0 - 1 + r, xx = x0 - 1 + col;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = *reinterpret_cast<const uint4*>(base + (static_cast<long long>(yy) * W + xx) * 64 + k * 8);
+        *reinterpret_cast<uint4*>(tile + ((r * 130 + col) * 8 + (k ^ (col & 7))) * 16) = v;
+    }
+    __syncthreads();
+    const int ty = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float acc[4][CO];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int o = 0; o < CO; ++o) acc[p][o] = bias ? bias[o] : 0.f;
+#pragma unroll 1
+    for (int t = 0; t < 9; ++t) {
+        const int dy = t / 3, dx = t % 3;
+#pragma unroll 2
+        for (int k = 0; k < 8; ++k) {
+            float wv[8][4];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 q = ws[t][k * 8 + j];
+                wv[j][0] = q.x;
+                wv[j][1] = q.y;
+                wv[j][2] = q.z;
+                wv[j][3] = q.w;
+            }
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const int col = p * 32 + lane + dx;
+                float v[8];
+                unpack8(*reinterpret_cast<const uint4*>(tile + (((ty + dy) * 130 + col) * 8 + (k ^ (col & 7))) * 16), v);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int o = 0; o < CO; ++o) acc[p][o] = fmaf(v[j], wv[j][o], acc[p][o]);
+            }
+        }
+    }
+    const int y = y0 + ty;
+    if (y >= H) return;
+    uint8_t* ob = out + (static_cast<long long>(img_map ? img_map[n] : n) * H + y) * W * CO;
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+        const int x = x0 + p * 32 + lane;
+        if (x >= W) continue;
+#pragma unroll
+        for (int o = 0; o < CO; ++o)
+            ob[static_cast<long long>(x) * CO + o] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(acc[p][o], 0.f), 1.f) * 255.f));
+    }
+}
+
 // ---- timestep embedding ------------------------------------------------------------
 
 __global__ void temb_kernel(const int* taus, int n, int dim, bf16* out) {
@@ -937,6 +1022,18 @@ void run_conv3x3_rgb8(const uint8_t* in, long long img_stride, const int* img_sr
     if (ldw < 27) raise(SDX_INVALID_ARGUMENT, "conv3x3_rgb8: weight row shorter than 27");
     launch_pdl(conv3x3_rgb8_kernel, dim3((W + 255) / 256, H, imgs), dim3(256), 0, st, in, img_stride, img_src, H, W, w,
                ldw, bias, out, rows_dev);
+}
+
+void run_conv3x3_c64_u8(const bf16* in, int imgs, int H, int W, const bf16* w, int Cout, const float* bias,
+                        uint8_t* out, const int* img_map, const int* rows_dev, cudaStream_t st) {
+    if (Cout != 3) raise(SDX_INVALID_ARGUMENT, "conv3x3_c64_u8: 3 output channels");
+    static const bool attr = [] {
+        SDX_CUDA(cudaFuncSetAttribute(conv3x3_c64_u8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadTileBytes));
+        return true;
+    }();
+    (void)attr;
+    launch_pdl(conv3x3_c64_u8_kernel<3>, dim3((W + 127) / 128, (H + kHeadRows - 1) / kHeadRows, imgs), dim3(32 * kHeadRows),
+               static_cast<size_t>(kHeadTileBytes), st, in, H, W, w, bias, out, img_map, rows_dev);
 }
 
 void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStream_t st) {

@@ -66,6 +66,11 @@ void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_sr
 
 // Direct 3x3 / pad 1 conv of u8 NHWC RGB frames (scaled 1/255) to 64 bf16 channels:
 // w [64][ldw] bf16 with column k = tap * 3 + c (k < 27), bias [64] or null.
+// 3x3 conv (pad 1) from 64 channels NHWC bf16 to Cout = 3 channels, u8 output
+// round(255 clamp(v, 0, 1)), image n written to output image img_map[n] (TAESD decoder head).
+// w [Cout][3][3][64] bf16, bias fp32 (or null); images >= *rows_dev skipped.
+void run_conv3x3_c64_u8(const bf16* in, int imgs, int H, int W, const bf16* w, int Cout, const float* bias,
+                        uint8_t* out, const int* img_map, const int* rows_dev, cudaStream_t st);
 void run_conv3x3_rgb8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W,
                       const bf16* w, int ldw, const float* bias, bf16* out, const int* rows_dev, cudaStream_t st);
 

@@ -153,18 +153,14 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
                 cur = block(dec_, dec_flops_, r, cur, "dec.b" + std::to_string(r) + std::to_string(j), cnt);
         }
         {
-            GemmEpilogue e;
-            e.bias = wf32("dec.conv_out.b", {3}, 0.02f);
-            e.out = io.frames_out;
-            e.out_f32 = 2;  // u8 frame
-            e.ld_out = 3;
-            e.out_img_map = io.dec_dst;
-            e.rows_per_img = 512 * 512;
-            e.rows_dev = cnt;
-            e.rows_per_unit = 512 * 512;
-            bf16* w = wbf("dec.conv_out.w", {3, 3, 3, kC}, std::sqrt(1.f / (9.f * kC)));
-            GemmPlan p = plan_conv3x3(buf(0, cur), imax_, 512, 512, kC, w, 3, 1, e);
-            dec_.push_back(Op{"conv_out", [p](cudaStream_t s) { run_gemm(p, s); }});
+            // 64 -> 3 head as a CUDA-core conv (a tensor-core tile would pad N to 64)
+            const float* b = wf32("dec.conv_out.b", {3}, 0.02f);
+            const bf16* w = wbf("dec.conv_out.w", {3, 3, 3, kC}, std::sqrt(1.f / (9.f * kC)));
+            const bf16* x = buf(0, cur);
+            uint8_t* fo = io.frames_out;
+            const int* map = io.dec_dst;
+            const int im = imax_;
+            dec_.push_back(Op{"conv_out", [=](cudaStream_t s) { run_conv3x3_c64_u8(x, im, 512, 512, w, 3, b, fo, map, cnt, s); }});
             dec_flops_ += 2.0 * 512 * 512 * 3 * 9.0 * kC;
         }
     }
