@@ -103,16 +103,18 @@ __global__ void __launch_bounds__(320, 1)
     attn_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, AttnArgs a) {
     // Work unit -> (image, head, first q tile, tiles).  Pair units (two 128-query tiles sharing
     // every K/V block) cover the full waves; a remainder that would leave most SMs idle in a
-    // last wave runs as single-tile units in a second launch (a.single).
+    // last wave runs as single-tile units: CTAs >= a.pair_base of the same launch (the block
+    // scheduler issues them after the pair CTAs, so they fill the tail).
     const int npairs = (a.q_len + 2 * BQ - 1) / (2 * BQ);
-    const int lin = static_cast<int>(blockIdx.x) + a.unit_base;
-    const int plin = a.single ? a.pair_base + lin / 2 : lin;  // linear pair index, q pair fastest
+    const bool single = static_cast<int>(blockIdx.x) >= a.pair_base;
+    const int lin = single ? static_cast<int>(blockIdx.x) - a.pair_base : static_cast<int>(blockIdx.x);
+    const int plin = single ? a.pair_base + lin / 2 : lin;  // linear pair index, q pair fastest
     const int qp = plin % npairs;
     const int head = (plin / npairs) % a.heads;
     const int img = plin / (npairs * a.heads);
-    const int q_first = qp * 2 * BQ + (a.single ? (lin & 1) * BQ : 0);  // first query of this unit
+    const int q_first = qp * 2 * BQ + (single ? (lin & 1) * BQ : 0);  // first query of this unit
     if (threadIdx.x == 0) pdl_launch();
-    const bool has1 = !a.single && q_first + BQ < a.q_len;  // second tile holds live queries
+    const bool has1 = !single && q_first + BQ < a.q_len;  // second tile holds live queries
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -437,16 +439,11 @@ void run_attention(const AttnPlan& p, cudaStream_t st) {
     int full = total;
     if (total > kSmCount && (total % kSmCount) * 2 <= kSmCount)
         full = (total / kSmCount) * kSmCount;
+    // one launch: CTAs [0, full) run pair units, [full, full + 2 (total - full)) single-tile units
     a.single = 0;
     a.unit_base = 0;
-    a.pair_base = 0;
-    launch_pdl(attn_kernel, dim3(full), dim3(320), smem, st, p.tq, p.tkv, a);
-    if (full < total) {
-        a.single = 1;
-        a.pair_base = full;
-        const int units = 2 * (total - full);
-        launch_pdl(attn_kernel, dim3(units), dim3(320), smem, st, p.tq, p.tkv, a);
-    }
+    a.pair_base = full;
+    launch_pdl(attn_kernel, dim3(full + 2 * (total - full)), dim3(320), smem, st, p.tq, p.tkv, a);
 }
 
 }  // namespace sdx

@@ -19,7 +19,7 @@ struct AttnArgs {
     float scale;
     int xmode;                    // experiments only: 1 = no MMAs, 2 = no softmax math (pipeline probes)
     int heads;                    // set by run_attention
-    int single, unit_base, pair_base;  // launch split: pair units, then single-tile units
+    int single, unit_base, pair_base;  // CTAs >= pair_base run single-tile units (the tail); single/unit_base unused
 };
 
 // Pipeline probe for kernel experiments (results wrong): 0 off, 1 no MMAs, 2 no softmax math.
