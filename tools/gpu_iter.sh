@@ -1,11 +1,6 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1
-echo "rc=$?" >> gpurun_out/pytest_gpu.txt
-timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/smoke.txt 2>&1
-timeout 600 python bench.py > gpurun_out/bench_cfg1.json 2> gpurun_out/bench_cfg1.err
-timeout 600 python bench.py --streams 8 --n-steps 1 --guidance self_negative --no-cpu-baseline > gpurun_out/bench_cfg4.json 2> gpurun_out/bench_cfg4.err
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 300 python tools/prof_ops.py 4 > gpurun_out/prof_ops_r4.txt 2>&1
-timeout 300 python tools/prof_ops.py 8 > gpurun_out/prof_ops_r8.txt 2>&1
-bash tools/gpu_profile_round.sh > gpurun_out/profile_round.log 2>&1
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_kernels_gpu.py -m gpu -x -q -k "attention or tilings or conv3x3_halo" > gpurun_out/memcheck_kernels.txt 2>&1
+echo "rc=$?" >> gpurun_out/memcheck_kernels.txt
+timeout 1500 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_unet_gpu.py -m gpu -x -q > gpurun_out/memcheck_unet.txt 2>&1
+echo "rc=$?" >> gpurun_out/memcheck_unet.txt
