@@ -1,4 +1,5 @@
 cd "${GRAFT_REPO_ROOT:-.}"
 mkdir -p gpurun_out
-timeout 2400 compute-sanitizer --tool memcheck --print-limit 20 python -m pytest tests/test_pipeline_gpu.py tests/test_pipeline_unet_gpu.py -m gpu -x -q > gpurun_out/memcheck_pipeline.txt 2>&1
-echo "rc=$?" >> gpurun_out/memcheck_pipeline.txt
+timeout 900 python -m pytest tests/test_unet_gpu.py tests/test_pipeline_unet_gpu.py -m gpu -x -q > gpurun_out/t_all.txt 2>&1
+timeout 300 python tools/prof_ops.py 4 > gpurun_out/prof_ops_r4.txt 2>&1
+timeout 300 python tools/prof_ops.py 8 > gpurun_out/prof_ops_r8.txt 2>&1
