@@ -169,9 +169,23 @@ int sdx_pipeline_create(const sdx_pipeline_config* cfg, const sdx_step* steps,
                         const double* eps_cached, const double* cond, const double* neg,
                         int device, sdx_pipeline** out);
 int sdx_pipeline_destroy(sdx_pipeline* p);
-/* frames: S x frame_bytes host u8 (pinned memory from sdx_host_alloc avoids a
- * staging copy). */
+/* frames: S x frame_bytes host u8.  Pinned memory (sdx_host_alloc) is copied to
+ * HBM in place instead of through a staging buffer; either way the call returns
+ * only after the frames have been read, so the caller may refill its buffer at
+ * once.  The frames get the source sequence ids 0,1,2,... in push order. */
 int sdx_pipeline_push(sdx_pipeline* p, const uint8_t* frames);
+/* As push, with the S frames' source sequence ids (Frame::seq_id, pipeline.cpp:176):
+ * sink frames, duplicates and the trace carry these ids.  Per stream the ids of
+ * processed frames must strictly increase (engine.cpp:59-60, else the stream is
+ * flagged incomplete with the reference's message); gaps are allowed (input drops). */
+int sdx_pipeline_push_seq(sdx_pipeline* p, const uint8_t* frames, const int64_t* seq_ids);
+/* Live loop without input (pipeline.cpp:235-245 ticks whenever the engine is not
+ * idle): runs one frame-less iteration (a tick, no ingest) unless every stream is
+ * known to be idle; *ran tells which. */
+int sdx_pipeline_tick(sdx_pipeline* p, int* ran);
+/* *idle = 1 when no stream has a frame in flight (processed iterations only count
+ * once the device finished them; unfinished frame pushes count as busy). */
+int sdx_pipeline_idle(sdx_pipeline* p, int* idle);
 /* Source exhausted: keep ticking until every engine is idle, flush skips. */
 int sdx_pipeline_finish(sdx_pipeline* p);
 /* Next sink frame of stream s in sink order; *has = 0 when none is ready.

@@ -87,7 +87,7 @@ struct DevicePipeline {
     ~DevicePipeline() {
         if (p) sdx_pipeline_destroy(p);
     }
-    void push(const std::vector<std::uint8_t>& u8) {
+    void push(const std::vector<std::uint8_t>& u8, std::int64_t seq_id) {
         if (!p) {
             frame_bytes = static_cast<int64_t>(u8.size());
             sdx_pipeline_config pc{};
@@ -102,7 +102,14 @@ struct DevicePipeline {
             out_buf.resize(taesd ? static_cast<size_t>(frame_bytes) : static_cast<size_t>(cfg.d_latent) * 4);
         }
         if (static_cast<int64_t>(u8.size()) != frame_bytes) throw std::invalid_argument("ingest: latent length != d_latent");
-        check(sdx_pipeline_push(p, u8.data()));
+        check(sdx_pipeline_push_seq(p, u8.data(), &seq_id));
+    }
+    // a tick without input while frames are in flight; false when idle (nothing launched)
+    bool tick() {
+        if (!p) return false;
+        int ran = 0;
+        check(sdx_pipeline_tick(p, &ran));
+        return ran != 0;
     }
     // every output frame the pipeline has ordered so far, in sequence order
     template <class F>
@@ -172,7 +179,7 @@ inline MetricsReport run_pipeline(const EngineConfig& raw_cfg, FrameSource sourc
     if (!opts.threaded) {
         try {
             while (auto f = source()) {
-                dp.push(detail::to_u8(f->payload));
+                dp.push(detail::to_u8(f->payload), f->seq_id);
                 dp.drain([&](Frame&& o) { sink(o); });
             }
             dp.finish();
@@ -204,16 +211,24 @@ inline MetricsReport run_pipeline(const EngineConfig& raw_cfg, FrameSource sourc
         });
         std::thread engine([&] {
             try {
+                bool busy = false;  // frames may be in flight: tick without waiting for input
                 while (true) {
-                    // freshest-wins unless strict FIFO (pipeline.cpp:236-241)
-                    auto item = in_q.wait_dequeue(!opts.strict_fifo, std::chrono::microseconds(200));
+                    // freshest-wins unless strict FIFO (pipeline.cpp:236-241); block only when idle
+                    std::optional<InputItem> item;
+                    if (busy) item = opts.strict_fifo ? in_q.dequeue_fifo() : in_q.dequeue_latest();
+                    else item = in_q.wait_dequeue(!opts.strict_fifo, std::chrono::microseconds(200));
                     if (item) {
-                        dp.push(item->u8);
+                        dp.push(item->u8, item->seq);
+                        busy = true;
                         dp.drain([&](Frame&& o) { out_q.enqueue(std::move(o)); });
                     } else if (in_q.closed() && in_q.empty()) {
                         dp.finish();
                         dp.drain([&](Frame&& o) { out_q.enqueue(std::move(o)); });
                         break;
+                    } else if (busy) {
+                        // no input waiting: the reference still ticks the non-idle engine
+                        busy = dp.tick();
+                        dp.drain([&](Frame&& o) { out_q.enqueue(std::move(o)); });
                     }
                 }
             } catch (...) {

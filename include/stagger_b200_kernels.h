@@ -100,6 +100,13 @@ int sdx_taesd_encode(sdx_taesd* t, const uint8_t* frames, int n, float* latents,
 int sdx_taesd_decode(sdx_taesd* t, const float* latents, int n, uint8_t* frames, void* stream);
 int sdx_taesd_param_count(sdx_taesd* t, int* n);
 int sdx_taesd_param(sdx_taesd* t, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32);
+/* Measured denoise loop for the bench tables: one CUDA graph of [TAESD encode of
+ * `frames` 512x512 frames, `calls` UNet forwards of `rows_per_call` rows, TAESD decode of
+ * `frames` frames] (random-init weights, seeded), replayed `iters` times; *ms_per_iter =
+ * device ms per replay (CUDA events).  Sequential denoising (engine.cpp:213-238) is
+ * (1, n, 1) per frame; wait-and-batch (engine.cpp:240-309) is (n, n, n) per n frames. */
+int sdx_bench_denoise_loop(int rows_per_call, int calls, int frames, int n_steps, int iters, uint64_t seed,
+                           int device, double* ms_per_iter);
 /* cudaProfilerStart / Stop around a region (for ncu --profile-from-start off). */
 int sdx_profiler_start(void);
 int sdx_profiler_stop(void);

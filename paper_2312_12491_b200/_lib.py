@@ -88,6 +88,9 @@ _sig = {
                                       C.POINTER(P)]),
     "sdx_pipeline_destroy": (C.c_int, [P]),
     "sdx_pipeline_push": (C.c_int, [P, C.c_void_p]),
+    "sdx_pipeline_push_seq": (C.c_int, [P, C.c_void_p, C.c_void_p]),
+    "sdx_pipeline_tick": (C.c_int, [P, C.POINTER(C.c_int)]),
+    "sdx_pipeline_idle": (C.c_int, [P, C.POINTER(C.c_int)]),
     "sdx_pipeline_finish": (C.c_int, [P]),
     "sdx_pipeline_pop": (C.c_int, [P, C.c_int, C.POINTER(C.c_int64), C.c_void_p, C.POINTER(C.c_int)]),
     "sdx_pipeline_report": (C.c_int, [P, C.c_int, C.POINTER(sdx_report)]),

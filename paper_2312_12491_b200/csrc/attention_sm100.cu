@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "attention_sm100.cuh"
 #include "common.cuh"
@@ -40,6 +41,7 @@ constexpr int KVS = PB == 2 ? 2 : 4;  // K/V ring depth
 // (190.7 vs 190.2 us, tools/attn_probe.py): the softmax warps, not the MMA order, set
 // the pace.
 constexpr int kSAhead = 1;
+constexpr int KVS_TS = 6;  // K/V ring of the TMEM-P kernel (no P buffers in smem)
 
 __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
     const uint32_t a = smem_u32(bar);
@@ -364,6 +366,295 @@ __global__ void __launch_bounds__(320, 1)
     }
 }
 
+// ---- P in TMEM (FA4-style TS-MMA) -------------------------------------------------------
+// tcgen05.mma with the A operand in tensor memory: D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+        "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+    float r;
+    asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+    return r;
+}
+// (d0, d1) = (a0, a1) * s + (c, c) on the packed fp32 pipe (FFMA2)
+__device__ __forceinline__ void ffma2_bc(float& d0, float& d1, float a0, float a1, float s, float c) {
+    asm("{\n\t.reg .b64 va, vs, vc, vd;\n\t"
+        "mov.b64 va, {%2, %3};\n\t"
+        "mov.b64 vs, {%4, %4};\n\t"
+        "mov.b64 vc, {%5, %5};\n\t"
+        "fma.rn.ftz.f32x2 vd, va, vs, vc;\n\t"
+        "mov.b64 {%0, %1}, vd;\n\t}"
+        : "=f"(d0), "=f"(d1)
+        : "f"(a0), "f"(a1), "f"(s), "f"(c));
+}
+// (d0, d1) += (a0, a1) (FADD2)
+__device__ __forceinline__ void fadd2_acc(float& d0, float& d1, float a0, float a1) {
+    asm("{\n\t.reg .b64 va, vd;\n\t"
+        "mov.b64 va, {%2, %3};\n\t"
+        "mov.b64 vd, {%0, %1};\n\t"
+        "add.rn.ftz.f32x2 vd, vd, va;\n\t"
+        "mov.b64 {%0, %1}, vd;\n\t}"
+        : "+f"(d0), "+f"(d1)
+        : "f"(a0), "f"(a1));
+}
+
+// Two 128-query tiles per CTA, as attn_kernel, with the FA4 data flow: the softmax
+// warps read S_t(j) from TMEM, write P_t(j) = exp2(...) as packed bf16 back into the
+// first 64 columns of the same TMEM region (tcgen05.st), and PV_t(j) reads P straight
+// from TMEM as the A operand (TS-MMA).  No P in shared memory, no proxy fence, no
+// wait for PV(j-1) before the exponentials.  The MMA warp issues, per tile, PV_t(j)
+// and then S_t(j+1) into the same columns (MMAs execute in issue order), so the
+// commit that releases S_t(j+1) to the softmax also certifies O_t through block j.
+// TMEM: S/P of tile t at columns 128 t, O of tile t at 256 + 64 t.
+__global__ void __launch_bounds__(320, 1)
+    attn_ts_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, AttnArgs a) {
+    const int npairs = (a.q_len + 2 * BQ - 1) / (2 * BQ);
+    const bool single = static_cast<int>(blockIdx.x) >= a.pair_base;
+    const int lin = single ? static_cast<int>(blockIdx.x) - a.pair_base : static_cast<int>(blockIdx.x);
+    const int plin = single ? a.pair_base + lin / 2 : lin;
+    const int qp = plin % npairs;
+    const int head = (plin / npairs) % a.heads;
+    const int img = plin / (npairs * a.heads);
+    const int q_first = qp * 2 * BQ + (single ? (lin & 1) * BQ : 0);
+    if (threadIdx.x == 0) pdl_launch();
+    const bool has1 = !single && q_first + BQ < a.q_len;
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sQ = smem;                        // 2 x 16 KB
+    uint8_t* sK = sQ + 2 * TILE_BYTES;         // KVS_TS x 16 KB
+    uint8_t* sV = sK + KVS_TS * TILE_BYTES;    // KVS_TS x 16 KB
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sV + KVS_TS * TILE_BYTES);
+    uint64_t* q_full = bars + 0;
+    uint64_t* kv_full = bars + 1;            // [KVS_TS]
+    uint64_t* kv_empty = kv_full + KVS_TS;   // [KVS_TS]
+    uint64_t* s_full = kv_empty + KVS_TS;    // [2] S_t(j) in TMEM (and O_t final through j-1)
+    uint64_t* p_full = s_full + 2;           // [2] P_t(j) in TMEM
+    uint64_t* o_full = p_full + 2;           // [2] O_t final
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nkv = (a.kv_len + BKV - 1) / BKV;
+    const int q_row0 = img * a.q_rows_per_img + q_first;
+    const int prompt = a.kv_index ? a.kv_index[img] : img;
+    const int kv_row0 = prompt * a.kv_rows_per_img;
+
+    if (threadIdx.x == 0) {
+        tma_prefetch(&tq);
+        tma_prefetch(&tkv);
+        mbar_init(q_full, 1);
+        for (int i = 0; i < KVS_TS; ++i) {
+            mbar_init(&kv_full[i], 1);
+            mbar_init(&kv_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s_full[i], 1);
+            mbar_init(&p_full[i], 4);  // one arrival per softmax warp
+            mbar_init(&o_full[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    pdl_wait();
+    const bool live = !(a.rows_dev && img >= *a.rows_dev);
+
+    if (!live) {
+    } else if (warp == 0) {
+        if (lane == 0) {
+            mbar_expect_tx(q_full, (has1 ? 2 : 1) * TILE_BYTES);
+            tma_load_2d(sQ, &tq, q_full, a.q_col0 + head * HD, q_row0);
+            if (has1) tma_load_2d(sQ + TILE_BYTES, &tq, q_full, a.q_col0 + head * HD, q_row0 + BQ);
+            for (int j = 0; j < nkv; ++j) {
+                const int b = j % KVS_TS;
+                wait_bar(&kv_empty[b], ((j / KVS_TS) & 1) ^ 1);
+                mbar_expect_tx(&kv_full[b], 2 * TILE_BYTES);
+                tma_load_2d(sK + b * TILE_BYTES, &tkv, &kv_full[b], a.k_col0 + head * HD, kv_row0 + j * BKV);
+                tma_load_2d(sV + b * TILE_BYTES, &tkv, &kv_full[b], a.v_col0 + head * HD, kv_row0 + j * BKV);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc_s = idesc_bf16(128, 128);
+            constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);  // B (= V) MN-major
+            const int ntile = has1 ? 2 : 1;
+            auto issue_s = [&](int t, int j) {
+                const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ + t * TILE_BYTES));
+                const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + (j % KVS_TS) * TILE_BYTES));
+#pragma unroll
+                for (int k = 0; k < HD / 16; ++k) umma_f16(tmem + t * 128, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
+                umma_commit(&s_full[t]);
+            };
+            auto issue_pv = [&](int t, int j) {
+                const uint32_t vbase = smem_u32(sV + (j % KVS_TS) * TILE_BYTES);
+#pragma unroll
+                for (int k = 0; k < BKV / 16; ++k)  // P: 16 keys = 8 packed columns per MMA
+                    umma_f16_ts(tmem + 256 + t * 64, tmem + t * 128 + 8 * k, desc_mnmajor_sw128(vbase + k * 2048, 0),
+                                idesc_o, (j > 0 || k != 0) ? 1u : 0u);
+            };
+            wait_bar(q_full, 0);
+            wait_bar(&kv_full[0], 0);
+            tc_fence_after();
+            for (int t = 0; t < ntile; ++t) issue_s(t, 0);
+            int np[2] = {0, ntile > 1 ? 0 : nkv};  // next PV block per tile
+            int released = 0;
+            const long long t0 = clock64();
+            while (released < nkv) {
+                bool progress = false;
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (np[t] < nkv && mbar_test(&p_full[t], np[t] & 1)) {
+                        tc_fence_after();
+                        issue_pv(t, np[t]);
+                        const int j1 = np[t] + 1;
+                        if (j1 < nkv) {
+                            wait_bar(&kv_full[j1 % KVS_TS], (j1 / KVS_TS) & 1);
+                            tc_fence_after();
+                            issue_s(t, j1);  // overwrites P_t(j): issued after PV_t(j), executed in order
+                        } else {
+                            umma_commit(&o_full[t]);
+                        }
+                        np[t] = j1;
+                        progress = true;
+                    }
+                }
+                const int done = np[0] < np[1] ? np[0] : np[1];
+                while (released < done) umma_commit(&kv_empty[released++ % KVS_TS]);
+                if (!progress && clock64() - t0 > (1LL << 34)) {
+                    printf("sdx attention(ts): MMA issue watchdog (block %d)\n", blockIdx.x);
+                    asm volatile("trap;");
+                }
+            }
+        }
+        __syncwarp();
+    } else {
+        const int t = (warp - 2) >> 2;  // q tile of this softmax warpgroup
+        const int q = warp & 3;         // TMEM lane quarter this warp may access
+        const int r = q * 32 + lane;
+        if (t == 0 || has1) {
+            const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
+            const uint32_t s_addr = tmem + lane_off + t * 128;
+            const uint32_t o_addr = tmem + lane_off + 256 + t * 64;
+            const float sl2 = a.scale * 1.4426950408889634f;
+            float m_used = -INFINITY, l0 = 0.f, l1 = 0.f;
+            for (int j = 0; j < nkv; ++j) {
+                wait_bar(&s_full[t], j & 1);
+                tc_fence_after();
+                uint32_t sr[128];
+                tmem_ld32_nowait(s_addr + 0, sr);
+                tmem_ld32_nowait(s_addr + 32, sr + 32);
+                tmem_ld32_nowait(s_addr + 64, sr + 64);
+                tmem_ld32_nowait(s_addr + 96, sr + 96);
+                tmem_wait_ld32(sr);
+                tmem_wait_ld32(sr + 32);
+                tmem_wait_ld32(sr + 64);
+                tmem_wait_ld32(sr + 96);
+                const int kv_valid = a.kv_len - j * BKV;
+                if (kv_valid < BKV) {  // partial last block: masked keys read as -inf
+#pragma unroll
+                    for (int i = 0; i < BKV; ++i)
+                        if (i >= kv_valid) sr[i] = 0xff800000u;
+                }
+                // row max: 4 chains of 3-input max, then a tree
+                float mx4[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) mx4[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[4 + k]));
+#pragma unroll
+                for (int i = 8; i < BKV; i += 8) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        mx4[k] = fmax3f(mx4[k], __uint_as_float(sr[i + k]), __uint_as_float(sr[i + 4 + k]));
+                }
+                const float m_row = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+                // lazy rescale (warp-uniform: the TMEM accesses are warp-collective): move the
+                // reference max only when some row's max grew by more than 2^8
+                if (__any_sync(0xffffffffu, m_row > m_used + 8.f)) {
+                    const float m_new = fmaxf(m_used, m_row);
+                    const float corr = ex2(m_used - m_new);  // m_used = -inf -> 0
+                    if (j > 0) {
+                        // O_t is final through block j-1: s_full(j) was committed after PV_t(j-1)
+#pragma unroll
+                        for (int c = 0; c < HD; c += 16) {
+                            float v[16];
+                            tmem_ld16(o_addr + c, v);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i) v[i] *= corr;
+                            tmem_st16(o_addr + c, v);
+                        }
+                    }
+                    l0 *= corr;
+                    l1 *= corr;
+                    m_used = m_new;
+                }
+                // P = exp2(s * scale_log2 - m_used) as packed bf16 into TMEM (exp2(-inf) = 0)
+                const float nm = -m_used;
+#pragma unroll
+                for (int c = 0; c < BKV; c += 32) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        float x0, x1;
+                        ffma2_bc(x0, x1, __uint_as_float(sr[c + i]), __uint_as_float(sr[c + i + 1]), sl2, nm);
+                        const float p0 = ex2(x0), p1 = ex2(x1);
+                        fadd2_acc(l0, l1, p0, p1);
+                        pk[i / 2] = pack_bf16(p0, p1);
+                    }
+                    tmem_st16u(s_addr + (c >> 1), pk);
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&p_full[t]);
+            }
+            wait_bar(&o_full[t], 0);
+            tc_fence_after();
+            const int qi = q_first + t * BQ + r;
+            float o[HD];
+#pragma unroll
+            for (int c = 0; c < HD; c += 16) tmem_ld16(o_addr + c, o + c);
+            if (qi < a.q_len) {
+                const float inv = 1.f / (l0 + l1);
+                __nv_bfloat16* op = a.out + static_cast<long long>(q_row0 + t * BQ + r) * a.ld_out + a.out_col0 + head * HD;
+#pragma unroll
+                for (int c = 0; c < HD; c += 8) {
+                    uint4 w;
+                    w.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
+                    w.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
+                    w.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
+                    w.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
+                    *reinterpret_cast<uint4*>(op + c) = w;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -422,13 +713,20 @@ int g_attn_xmode = 0;
 }
 void set_attention_probe_mode(int mode) { g_attn_xmode = mode; }
 
+// SDX_ATTN_TS=0: the P-in-shared-memory kernel (attn_kernel) instead of attn_ts_kernel
+static bool attn_ts_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("SDX_ATTN_TS");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 void run_attention(const AttnPlan& p, cudaStream_t st) {
-    static bool attr = false;
-    const size_t smem = (2 + 2 * KVS + 4 * PB) * TILE_BYTES + 1024 + 256;
-    if (!attr) {
-        SDX_CUDA(cudaFuncSetAttribute(attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
+    const bool ts = attn_ts_enabled() && g_attn_xmode == 0;
+    const size_t smem = ts ? (2 + 2 * KVS_TS) * TILE_BYTES + 1024 + 256 : (2 + 2 * KVS + 4 * PB) * TILE_BYTES + 1024 + 256;
+    if (ts) ensure_kernel_attrs(attn_ts_kernel, smem);
+    else ensure_kernel_attrs(attn_kernel, smem);
     AttnArgs a = p.a;
     a.xmode = g_attn_xmode;
     a.heads = p.heads;
@@ -443,7 +741,7 @@ void run_attention(const AttnPlan& p, cudaStream_t st) {
     a.single = 0;
     a.unit_base = 0;
     a.pair_base = full;
-    launch_pdl(attn_kernel, dim3(full + 2 * (total - full)), dim3(320), smem, st, p.tq, p.tkv, a);
+    launch_pdl(ts ? attn_ts_kernel : attn_kernel, dim3(full + 2 * (total - full)), dim3(320), smem, st, p.tq, p.tkv, a);
 }
 
 }  // namespace sdx

@@ -182,6 +182,28 @@ int sdx_pipeline_push(sdx_pipeline* p, const uint8_t* frames) {
         p->impl.push(frames);
     });
 }
+int sdx_pipeline_push_seq(sdx_pipeline* p, const uint8_t* frames, const int64_t* seq_ids) {
+    return guarded([&] {
+        NEED(p);
+        NEED(frames);
+        NEED(seq_ids);
+        p->impl.push(frames, seq_ids);
+    });
+}
+int sdx_pipeline_tick(sdx_pipeline* p, int* ran) {
+    return guarded([&] {
+        NEED(p);
+        const bool r = p->impl.tick_idle();
+        if (ran) *ran = r ? 1 : 0;
+    });
+}
+int sdx_pipeline_idle(sdx_pipeline* p, int* idle) {
+    return guarded([&] {
+        NEED(p);
+        NEED(idle);
+        *idle = p->impl.idle() ? 1 : 0;
+    });
+}
 int sdx_pipeline_finish(sdx_pipeline* p) {
     return guarded([&] {
         NEED(p);

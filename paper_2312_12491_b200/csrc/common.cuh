@@ -5,6 +5,8 @@
 
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <utility>
 #include <stdexcept>
 #include <string>
@@ -59,6 +61,27 @@ inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
     cfg.attrs = at;
     cfg.numAttrs = 1;
     cuda_check(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...), "cudaLaunchKernelEx", __FILE__, __LINE__);
+}
+
+// Kernel attributes (dynamic smem above 48 KB, non-portable cluster sizes) belong
+// to a device context: set them once per (kernel, device), under a lock, before the
+// kernel's first launch on that device.  Pipelines on several GPUs in one process
+// and concurrent plan creation on several threads are both safe.
+template <typename... KArgs>
+inline void ensure_kernel_attrs(void (*kern)(KArgs...), size_t smem, bool nonportable_cluster = false) {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice", __FILE__, __LINE__);
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;  // value: smem set + 1
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{reinterpret_cast<const void*>(kern), dev}];
+    if (have > smem) return;
+    if (nonportable_cluster)
+        cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1),
+                   "cudaFuncSetAttribute", __FILE__, __LINE__);
+    cuda_check(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "cudaFuncSetAttribute", __FILE__, __LINE__);
+    have = smem + 1;
 }
 
 #ifdef __CUDACC__

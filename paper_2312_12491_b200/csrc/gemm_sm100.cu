@@ -1048,12 +1048,8 @@ template <int BN, int AMODE, bool FAST, bool PAIR>
 void launch_t(const GemmPlan& p, cudaStream_t st) {
     constexpr int S = stages_for<BN, PAIR, AMODE, FAST>();
     auto k = gemm_tc_kernel<BN, S, AMODE, FAST, PAIR>;
-    static bool attr = false;
     const size_t smem = smem_for<BN, PAIR, AMODE, FAST>();
-    if (!attr) {
-        SDX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        attr = true;
-    }
+    ensure_kernel_attrs(k, smem);
     GemmArgs g{};
     g.M = p.M;
     g.N = p.N;

@@ -11,6 +11,7 @@
 #include "stagger_b200_kernels.h"
 #include "taesd.cuh"
 #include "unet.cuh"
+#include <memory>
 #include <numeric>
 #include <vector>
 
@@ -411,4 +412,75 @@ extern "C" {
 // Bracket a region for `ncu --profile-from-start off` (bench.py --profile-window).
 int sdx_profiler_start(void) { return kguard([&] { SDX_CUDA(cudaProfilerStart()); }); }
 int sdx_profiler_stop(void) { return kguard([&] { SDX_CUDA(cudaProfilerStop()); }); }
+
+// Measured denoise loops for the bench tables (bench.cpp:225-244, engine.cpp:213-309):
+// one CUDA graph of [TAESD encode of `frames` frames, `calls` UNet calls of
+// `rows_per_call` rows, TAESD decode of `frames` frames], replayed `iters` times and
+// timed with CUDA events.  sequential = (1 row, n calls, 1 frame) per frame;
+// wait-and-batch = (n rows, n calls, n frames) per n frames.
+int sdx_bench_denoise_loop(int rows_per_call, int calls, int frames, int n_steps, int iters, uint64_t seed,
+                           int device, double* ms_per_iter) {
+    return kguard([&] {
+        if (rows_per_call < 1 || calls < 1 || frames < 1 || n_steps < 1 || iters < 1 || !ms_per_iter)
+            sdx::raise(SDX_INVALID_ARGUMENT, "bench_denoise_loop: bad arguments");
+        SDX_CUDA(cudaSetDevice(device));
+        std::vector<sdx_step> steps(static_cast<size_t>(n_steps));
+        if (sdx_build_schedule(n_steps, 1000, 1.0, steps.data()) != 0)
+            sdx::raise(SDX_INVALID_ARGUMENT, sdx_precompute_error());
+        sdx::UNetConfig c;
+        c.rmax = rows_per_call;
+        for (const auto& s : steps) c.taus.push_back(s.tau);
+        c.seed = seed;
+        sdx_taesd* t = nullptr;
+        if (sdx_taesd_create(frames, seed ^ 0x7AE5DULL, device, &t) != SDX_OK) sdx::raise(SDX_CUDA_ERROR, g_kerr);
+        std::unique_ptr<sdx_taesd, int (*)(sdx_taesd*)> tguard(t, sdx_taesd_destroy);
+        sdx::UNet net(c, nullptr);
+        int* d_rows = sdx::dev_alloc<int>(1);
+        std::vector<int> hs(static_cast<size_t>(rows_per_call)), hp(static_cast<size_t>(rows_per_call), 0);
+        for (int r = 0; r < rows_per_call; ++r) hs[static_cast<size_t>(r)] = r % n_steps;
+        SDX_CUDA(cudaMemcpy(net.row_step(), hs.data(), sizeof(int) * hs.size(), cudaMemcpyHostToDevice));
+        SDX_CUDA(cudaMemcpy(net.row_prompt(), hp.data(), sizeof(int) * hp.size(), cudaMemcpyHostToDevice));
+        SDX_CUDA(cudaMemcpy(d_rows, &rows_per_call, sizeof(int), cudaMemcpyHostToDevice));
+        SDX_CUDA(cudaMemcpy(t->enc_cnt, &frames, sizeof(int), cudaMemcpyHostToDevice));
+        SDX_CUDA(cudaMemcpy(t->dec_cnt, &frames, sizeof(int), cudaMemcpyHostToDevice));
+        SDX_CUDA(cudaMemset(t->frames_in, 77, 512ull * 512 * 3 * frames));
+        const size_t lat = 64ull * 64 * 4 * sizeof(float);
+        const size_t moved = lat * static_cast<size_t>(std::min(rows_per_call, frames));
+        cudaStream_t st = nullptr;
+        SDX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        auto body = [&] {
+            t->t->encode(st);
+            SDX_CUDA(cudaMemcpyAsync(net.input(), t->lat_out, moved, cudaMemcpyDeviceToDevice, st));
+            for (int i = 0; i < calls; ++i) net.forward(d_rows, st);
+            SDX_CUDA(cudaMemcpyAsync(t->lat_in, net.output(), moved, cudaMemcpyDeviceToDevice, st));
+            t->t->decode(st);
+        };
+        body();  // plans, first-launch attributes
+        SDX_CUDA(cudaStreamSynchronize(st));
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        SDX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        body();
+        SDX_CUDA(cudaStreamEndCapture(st, &g));
+        SDX_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        for (int i = 0; i < 3; ++i) SDX_CUDA(cudaGraphLaunch(ge, st));
+        cudaEvent_t e0, e1;
+        SDX_CUDA(cudaEventCreate(&e0));
+        SDX_CUDA(cudaEventCreate(&e1));
+        SDX_CUDA(cudaEventRecord(e0, st));
+        for (int i = 0; i < iters; ++i) SDX_CUDA(cudaGraphLaunch(ge, st));
+        SDX_CUDA(cudaEventRecord(e1, st));
+        SDX_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        SDX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        *ms_per_iter = static_cast<double>(ms) / iters;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        cudaStreamDestroy(st);
+        sdx::dev_free(d_rows);
+    });
+}
+
 }

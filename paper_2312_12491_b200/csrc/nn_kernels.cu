@@ -932,12 +932,7 @@ void run_groupnorm(const GnPlan& p, cudaStream_t st) {
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
     if (p.cluster) {
-        static const bool attr = [] {
-            SDX_CUDA(cudaFuncSetAttribute(gn_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-            SDX_CUDA(cudaFuncSetAttribute(gn_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kGnBufBytes));
-            return true;
-        }();
-        (void)attr;
+        ensure_kernel_attrs(gn_cluster_kernel, 2 * kGnBufBytes, /*nonportable_cluster=*/true);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(p.cluster, p.imgs);
         cfg.blockDim = dim3(noct * std::max(1, 320 / noct));
@@ -1027,11 +1022,7 @@ void run_conv3x3_rgb8(const uint8_t* in, long long img_stride, const int* img_sr
 void run_conv3x3_c64_u8(const bf16* in, int imgs, int H, int W, const bf16* w, int Cout, const float* bias,
                         uint8_t* out, const int* img_map, const int* rows_dev, cudaStream_t st) {
     if (Cout != 3) raise(SDX_INVALID_ARGUMENT, "conv3x3_c64_u8: 3 output channels");
-    static const bool attr = [] {
-        SDX_CUDA(cudaFuncSetAttribute(conv3x3_c64_u8_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kHeadTileBytes));
-        return true;
-    }();
-    (void)attr;
+    ensure_kernel_attrs(conv3x3_c64_u8_kernel<3>, kHeadTileBytes);
     launch_pdl(conv3x3_c64_u8_kernel<3>, dim3((W + 127) / 128, (H + kHeadRows - 1) / kHeadRows, imgs), dim3(32 * kHeadRows),
                static_cast<size_t>(kHeadTileBytes), st, in, H, W, w, bias, out, img_map, rows_dev);
 }

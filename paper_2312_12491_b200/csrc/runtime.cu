@@ -777,15 +777,15 @@ void Pipeline::run_iteration(int k, bool frame_present) {
         run_encode(k);
         SDX_CUDA(cudaStreamWaitEvent(stream_, enc_done_[static_cast<size_t>(k)], 0));
     }
-    const bool use_graph = cfg_.graph && frame_present && !profile_;
+    const bool use_graph = cfg_.graph && !profile_;
     if (!use_graph) {
         launch_iteration(k, frame_present);
     } else {
-        // one graph per (ring slot, output-copy variant): pointers differ per slot
-        const int key = k * 2 + ((!resident_ || copy_outputs_) ? 1 : 0);
-        if (graphs_.size() < static_cast<size_t>(2 * K_)) {
-            graphs_.assign(static_cast<size_t>(2 * K_), nullptr);
-            graph_launches_.assign(static_cast<size_t>(2 * K_), 0);
+        // one graph per (ring slot, output-copy variant, frame present): pointers differ per slot
+        const int key = (k * 2 + ((!resident_ || copy_outputs_) ? 1 : 0)) * 2 + (frame_present ? 1 : 0);
+        if (graphs_.size() < static_cast<size_t>(4 * K_)) {
+            graphs_.assign(static_cast<size_t>(4 * K_), nullptr);
+            graph_launches_.assign(static_cast<size_t>(4 * K_), 0);
         }
         if (!graphs_[static_cast<size_t>(key)]) {
             const long long before = launches_;
@@ -841,17 +841,33 @@ std::shared_ptr<std::vector<uint8_t>> Pipeline::acquire_buffer() {
     return pool_.back();
 }
 
+int64_t Pipeline::src_of(const StreamHost& h, int64_t dev_seq) {
+    return h.src_ids[static_cast<size_t>(dev_seq - h.src_base)];
+}
+
+// Drop the source ids no future output can refer to: below every pending skip,
+// every in-flight frame and every frame not yet processed.
+void Pipeline::trim_src(StreamHost& h) {
+    int64_t keep = static_cast<int64_t>(h.frames_in);
+    if (!h.pending_skips.empty()) keep = std::min(keep, h.pending_skips.front());
+    keep = std::min(keep, h.eng->min_inflight_seq());
+    while (h.src_base < keep && !h.src_ids.empty()) {
+        h.src_ids.pop_front();
+        h.src_base += 1;
+    }
+}
+
 void Pipeline::flush_below(StreamHost& h, int64_t limit, std::vector<Out>& staged) {
-    // EngineStage::flush_skips_below (pipeline.cpp:102-116)
+    // EngineStage::flush_skips_below (pipeline.cpp:102-116); limit is a device frame index
     while (!h.pending_skips.empty() && h.pending_skips.front() < limit) {
         const int64_t seq = h.pending_skips.front();
         h.pending_skips.pop_front();
-        if (!h.last_output) {
+        if (!h.has_output) {
             h.stale += 1;
             continue;
         }
         h.duplicates += 1;
-        staged.push_back(Out{seq, h.last_output});
+        staged.push_back(Out{src_of(h, seq), h.last_output});
     }
 }
 
@@ -886,17 +902,28 @@ void Pipeline::process(int k, bool frame_present) {
                 if (skip) h.skipped += 1;
                 h.decisions.push_back(L.decision);
             }
-            if (skip) h.pending_skips.push_back(L.seq_in);
-            else h.eng->ingest(L.seq_in);
+            if (skip) {
+                h.pending_skips.push_back(L.seq_in);
+            } else {
+                // StreamBatchEngine::ingest (engine.cpp:59-60) on the source id
+                const int64_t src = src_of(h, L.seq_in);
+                if (src <= h.last_src) {
+                    h.incomplete = true;
+                    h.error = "ingest: seq ids must strictly increase";
+                    continue;
+                }
+                h.last_src = src;
+                h.eng->ingest(L.seq_in);
+            }
         }
         const bool ingested_now = frame_present && !(e.ssf_enabled && L.decision == SDX_GATE_SKIP);
         if (!h.eng->idle()) {
             const uint64_t calls0 = h.eng->calls, evals0 = h.eng->evals;
             const auto t = h.eng->tick();
             if (h.trace.size() < (size_t(1) << 20))
-                h.trace.push_back(sdx_trace_entry{h.eng->ticks(), ingested_now ? static_cast<int64_t>(L.seq_in) : -1,
-                                                  t.emitted ? t.seq : -1, h.eng->calls - calls0, h.eng->evals - evals0,
-                                                  iter_ns});
+                h.trace.push_back(sdx_trace_entry{h.eng->ticks(), ingested_now ? src_of(h, L.seq_in) : -1,
+                                                  t.emitted ? src_of(h, t.seq) : -1, h.eng->calls - calls0,
+                                                  h.eng->evals - evals0, iter_ns});
             if (t.emitted != (L.emit_seq >= 0) || (t.emitted && t.seq != L.emit_seq)) {
                 h.incomplete = true;
                 h.error = "device/host engine mirror diverged";
@@ -917,10 +944,12 @@ void Pipeline::process(int k, bool frame_present) {
                 }
                 h.lats.push_back(t.emit_tick - t.ingest_tick);
                 h.last_output = payload;
-                staged.push_back(Out{t.seq, payload});
+                h.has_output = true;
+                staged.push_back(Out{src_of(h, t.seq), payload});
             }
         }
         flush_below(h, h.eng->min_inflight_seq(), staged);
+        trim_src(h);
         // out_q: bounded drop-oldest (queue.hpp:23-34), drained every iteration
         size_t first = 0;
         if (staged.size() > cap8) {
@@ -950,7 +979,7 @@ void Pipeline::drain_completed(bool block_all) {
     }
 }
 
-void Pipeline::push(const uint8_t* frames) {
+void Pipeline::push(const uint8_t* frames, const int64_t* seq_ids) {
     SDX_CUDA(cudaSetDevice(device_));
     const int k = static_cast<int>(iter_ % K_);
     while (static_cast<int>(inflight_.size()) >= K_) {
@@ -959,6 +988,13 @@ void Pipeline::push(const uint8_t* frames) {
         process(kk, fp);
         inflight_.pop_front();
     }
+    for (int s = 0; s < S_; ++s) {
+        // the device numbers each stream's frames 0,1,2,... (ctl_begin_kernel); the
+        // source ids are mapped back when the host orders the sink
+        StreamHost& h = st_[static_cast<size_t>(s)];
+        h.src_ids.push_back(seq_ids ? seq_ids[s] : frames_pushed_);
+    }
+    frames_pushed_ += 1;
     if (frames) {
         resident_ = false;
         const uint8_t* src = frames;
@@ -979,6 +1015,9 @@ void Pipeline::push(const uint8_t* frames) {
                                        cudaMemcpyHostToDevice, copy_));
         }
         SDX_CUDA(cudaEventRecord(h2d_[static_cast<size_t>(k)], copy_));
+        // a pinned caller buffer is read in place: return only once the copy is done,
+        // so the caller may refill it right away (the copy is not queued behind compute)
+        if (pinned) SDX_CUDA(cudaEventSynchronize(h2d_[static_cast<size_t>(k)]));
     } else {
         // resident mode: frames already in ring slot k (upload_resident)
         SDX_CUDA(cudaEventRecord(h2d_[static_cast<size_t>(k)], stream_));
@@ -987,6 +1026,32 @@ void Pipeline::push(const uint8_t* frames) {
     inflight_.push_back({k, true});
     iter_ += 1;
     drain_completed(false);
+}
+
+bool Pipeline::idle() {
+    SDX_CUDA(cudaSetDevice(device_));
+    drain_completed(false);
+    for (const auto& [k, fp] : inflight_)
+        if (fp) return false;  // an unprocessed frame may have been ingested
+    for (const auto& h : st_)
+        if (!h.incomplete && !h.eng->idle()) return false;
+    return true;
+}
+
+bool Pipeline::tick_idle() {
+    if (idle()) return false;
+    const int k = static_cast<int>(iter_ % K_);
+    while (static_cast<int>(inflight_.size()) >= K_) {
+        const auto [kk, fp] = inflight_.front();
+        SDX_CUDA(cudaEventSynchronize(done_[static_cast<size_t>(kk)]));
+        process(kk, fp);
+        inflight_.pop_front();
+    }
+    run_iteration(k, false);
+    inflight_.push_back({k, false});
+    iter_ += 1;
+    drain_completed(false);
+    return true;
 }
 
 void Pipeline::upload_resident(const uint8_t* frames, int count) {

@@ -142,7 +142,14 @@ class Pipeline {
     Pipeline(const sdx_pipeline_config& cfg, const sdx_step* steps, const double* eps_cached,
              const double* cond, const double* neg, int device);
     ~Pipeline();
-    void push(const uint8_t* frames);
+    // seq_ids: the S source sequence ids of this push's frames (NULL: the frame index)
+    void push(const uint8_t* frames, const int64_t* seq_ids = nullptr);
+    // One frame-less iteration (a tick with no ingest) when some stream may still
+    // have frames in flight; returns false, without launching, when every stream is
+    // known to be idle.  The threaded live loop calls it when no input is waiting
+    // (pipeline.cpp:235-245 ticks whenever the engine is not idle).
+    bool tick_idle();
+    bool idle();
     void upload_resident(const uint8_t* frames, int count);
     void push_resident(bool copy_outputs);
     void finish();
@@ -175,7 +182,13 @@ class Pipeline {
     struct StreamHost {
         std::unique_ptr<EngineMirror> eng;
         std::deque<int64_t> pending_skips;
-        std::shared_ptr<std::vector<uint8_t>> last_output;
+        std::shared_ptr<std::vector<uint8_t>> last_output;  // null in the no-copy benchmark mode
+        bool has_output = false;  // EngineStage::last_output_ engaged (pipeline.cpp:106)
+        // source sequence ids by device frame index (the device numbers the frames of a
+        // stream 0,1,2,...); src_base is the device index of src_ids.front()
+        std::deque<int64_t> src_ids;
+        int64_t src_base = 0;
+        int64_t last_src = INT64_MIN;  // last ingested source id (engine.cpp:59-60)
         std::deque<Out> sink;
         std::vector<int64_t> lats;
         std::vector<int> decisions;
@@ -192,10 +205,12 @@ class Pipeline {
     void run_iteration(int k, bool frame_present);
     void join_decode();
     void process(int k, bool frame_present);
-    std::vector<cudaGraphExec_t> graphs_;     // [ring slot][output-copy variant]
+    std::vector<cudaGraphExec_t> graphs_;     // [ring slot][output-copy variant][frame present]
     std::vector<long long> graph_launches_;
     void drain_completed(bool block_all);
     void flush_below(StreamHost& h, int64_t limit, std::vector<Out>& staged);
+    static int64_t src_of(const StreamHost& h, int64_t dev_seq);
+    static void trim_src(StreamHost& h);
     std::shared_ptr<std::vector<uint8_t>> acquire_buffer();
     std::vector<std::shared_ptr<std::vector<uint8_t>>> pool_;
 
@@ -218,6 +233,7 @@ class Pipeline {
     std::vector<cudaEvent_t> done_;
     std::deque<std::pair<int, bool>> inflight_;  // (ring slot, frame_present)
     int64_t iter_ = 0;
+    int64_t frames_pushed_ = 0;  // frame-present iterations (the device frame index)
     std::vector<StreamHost> st_;
     cudaEvent_t t0_ = nullptr, t1_ = nullptr;
     bool profile_ = false;

@@ -361,11 +361,28 @@ class Pipeline:
 
     __del__ = close
 
-    def push(self, frames: np.ndarray):
+    def push(self, frames: np.ndarray, seq_ids=None):
+        """One iteration over the S streams' frames.  seq_ids (S source sequence ids,
+        pipeline.cpp:176) default to the frame index."""
         frames = np.ascontiguousarray(frames, dtype=np.uint8)
         if frames.size != self.S * self.D:
             raise InvalidArgument("LatentCodec::encode: dim mismatch")
-        _check(L.lib.sdx_pipeline_push(self._h, frames.ctypes.data))
+        if seq_ids is None:
+            _check(L.lib.sdx_pipeline_push(self._h, frames.ctypes.data))
+        else:
+            ids = np.ascontiguousarray(np.broadcast_to(np.asarray(seq_ids, dtype=np.int64), (self.S,)))
+            _check(L.lib.sdx_pipeline_push_seq(self._h, frames.ctypes.data, ids.ctypes.data))
+
+    def tick(self) -> bool:
+        """A frame-less iteration (tick without ingest) unless every stream is idle."""
+        ran = C.c_int()
+        _check(L.lib.sdx_pipeline_tick(self._h, C.byref(ran)))
+        return bool(ran.value)
+
+    def idle(self) -> bool:
+        v = C.c_int()
+        _check(L.lib.sdx_pipeline_idle(self._h, C.byref(v)))
+        return bool(v.value)
 
     def push_ptr(self, ptr: int):
         _check(L.lib.sdx_pipeline_push(self._h, C.c_void_p(ptr)))
@@ -456,15 +473,16 @@ class Pipeline:
         return v.value
 
 
-def run_pipeline(cfg: EngineConfig, frames: np.ndarray, max_skip: int = 0, device: int = 0):
-    """Deterministic run_pipeline over u8 frames [N, D] (vector_source order,
-    seq = index).  Returns (sink list of (seq, payload), report dict)."""
+def run_pipeline(cfg: EngineConfig, frames: np.ndarray, max_skip: int = 0, device: int = 0, seq_ids=None):
+    """Deterministic run_pipeline over u8 frames [N, D] (vector_source order;
+    seq = index unless seq_ids gives the source ids).  Returns (sink list of
+    (seq, payload), report dict)."""
     frames = np.ascontiguousarray(frames, dtype=np.uint8)
     p = Pipeline(cfg, 1, frames.shape[1], max_skip=max_skip, device=device)
     sink = []
     try:
-        for f in frames:
-            p.push(f)
+        for i, f in enumerate(frames):
+            p.push(f, None if seq_ids is None else [seq_ids[i]])
             sink.extend(p.pop_all(0))
         p.finish()
         sink.extend(p.pop_all(0))

@@ -244,7 +244,29 @@ static void runtime_pipeline() {
             CHECK(rep.element_evals == orep.element_evals && rep.ticks == orep.ticks);
             CHECK(rep.latency_ticks_max == orep.latency_ticks_max);
             if (kind == 0) CHECK(rep.ssf_skipped == 59 && rep.duplicates == 59);
+            // the sink carries the SOURCE's seq ids (pipeline.cpp:176), here 1000 + 3 i:
+            // same frames, same order, ids mapped through the source
+            std::vector<Frame> sparse = frames;
+            for (size_t i = 0; i < sparse.size(); ++i) sparse[i].seq_id = 1000 + 3 * std::int64_t(i);
+            std::vector<Frame> got2;
+            const auto rep2 = run_pipeline(cfg, vector_source(sparse), [&](const Frame& f) { got2.push_back(f); });
+            CHECK(!rep2.incomplete && got2.size() == got.size());
+            bool mapped = got2.size() == got.size();
+            for (size_t i = 0; mapped && i < got2.size(); ++i)
+                mapped = got2[i].seq_id == 1000 + 3 * got[i].seq_id && got2[i].payload == got[i].payload;
+            CHECK(mapped);
         }
+    }
+    // a processed frame whose source id does not increase -> ingest error, incomplete
+    // (engine.cpp:59-60 "ingest: seq ids must strictly increase")
+    {
+        EngineConfig cfg;
+        cfg.n_steps = 2;
+        cfg.d_latent = 256;
+        auto frames = u8_frames(1, 256, 5, 6);
+        frames[4].seq_id = 2;
+        const auto rep = run_pipeline(cfg, vector_source(frames), [](const Frame&) {});
+        CHECK(rep.incomplete && rep.error.find("strictly increase") != std::string::npos);
     }
     // byte-identical deterministic reports (test_runtime.cpp:228-242)
     EngineConfig cfg;
@@ -342,16 +364,22 @@ static void runtime_trace_and_threaded() {
         opts.threaded = true;
         opts.strict_fifo = false;  // freshest-wins
         std::vector<Frame> got;
-        const auto frames = u8_frames(2, 4096, 43, 300);
+        auto frames = u8_frames(2, 4096, 43, 300);
+        for (size_t i = 0; i < frames.size(); ++i) frames[i].seq_id = 7 + 5 * std::int64_t(i);
         const auto rep = run_pipeline(cfg, vector_source(frames), [&](const Frame& f) { got.push_back(f); }, opts);
         CHECK(!rep.incomplete);
         CHECK(rep.output_drops == 0);
         CHECK(rep.frames_in == 300);
         CHECK(rep.frames_out + rep.input_drops >= 300 - 2 * 4);
         CHECK(!got.empty());
-        bool inc = true;
+        bool inc = true, known = true;
         for (size_t i = 1; i < got.size(); ++i) inc = inc && got[i].seq_id > got[i - 1].seq_id;
+        // every sink id is one of the source's ids (input drops leave gaps, never renumber)
+        for (const auto& f : got) known = known && f.seq_id >= 7 && (f.seq_id - 7) % 5 == 0 && f.seq_id < 7 + 5 * 300;
         CHECK(inc);
+        CHECK(known);
+        // the last frame is never dropped by freshest-wins: it reaches the sink
+        CHECK(got.back().seq_id == 7 + 5 * 299);
     }
 }
 

@@ -172,3 +172,80 @@ def test_pipeline_cross_frame_attention(sg, orc, mode, n):
     frames = u8_stream("periodic", 256, 51 + n, 40)
     want, sink, rep = compare(sg, orc, frames, n, mode=mode, xfa=True)
     assert rep["latency_ticks_min"] == rep["latency_ticks_max"] == n
+
+
+def test_pipeline_source_seq_ids(sg, orc):
+    # the sink, duplicates and trace carry the source's Frame::seq_id (pipeline.cpp:176):
+    # sparse ids map one to one onto the frame-index run
+    D, n = 1024, 3
+    frames = u8_stream("periodic", D, 61, 70)
+    ids = [500 + 7 * i for i in range(len(frames))]
+    cfg = sg.EngineConfig(n_steps=n, ssf_enabled=True, seed=9, d_latent=D)
+    base, rep0 = sg.run_pipeline(cfg, frames)
+    sink, rep = sg.run_pipeline(cfg, frames, seq_ids=ids)
+    assert rep["duplicates"] == rep0["duplicates"] > 0
+    assert [s for s, _ in sink] == [ids[s] for s, _ in base]
+    for (_, a), (_, b) in zip(sink, base):
+        assert np.array_equal(a, b)
+    # trace ids are source ids as well
+    p = sg.Pipeline(cfg, 1, D)
+    for i, f in enumerate(frames):
+        p.push(f[None], [ids[i]])
+    p.finish()
+    ingested = {e["ingested"] for e in p.trace(0) if e["ingested"] is not None}
+    p.close()
+    assert ingested <= set(ids) and len(ingested) == len(frames) - rep["ssf_skipped"]
+
+
+def test_pipeline_seq_ids_must_increase(sg):
+    # engine.cpp:59-60: an ingested frame whose id does not increase fails the stream
+    D = 256
+    cfg = sg.EngineConfig(n_steps=2, d_latent=D)
+    frames = u8_stream("dynamic", D, 3, 6)
+    sink, rep = sg.run_pipeline(cfg, frames, seq_ids=[0, 1, 2, 3, 2, 5])
+    assert rep["incomplete"] and "strictly increase" in rep["error"]
+
+
+def test_pipeline_tick_without_input(sg, orc):
+    # pipeline.cpp:235-245: the live loop ticks a non-idle engine when no input waits; the
+    # frames in flight complete with latency n and the same payloads as a flushed run
+    D, n = 512, 4
+    frames = u8_stream("dynamic", D, 8, 3)
+    cfg = sg.EngineConfig(n_steps=n, seed=4, d_latent=D)
+    want, _ = sg.run_pipeline(cfg, frames)
+    p = sg.Pipeline(cfg, 1, D)
+    for f in frames:
+        p.push(f[None])
+    ran = 0
+    while p.tick():
+        ran += 1
+        assert ran < 50
+    assert p.idle()
+    got = p.pop_all(0)
+    rep = p.report(0)
+    p.close()
+    assert ran >= n - 1
+    assert [s for s, _ in got] == [s for s, _ in want]
+    for (_, a), (_, b) in zip(got, want):
+        assert np.array_equal(a, b)
+    assert rep["latency_ticks_min"] == rep["latency_ticks_max"] == n
+
+
+def test_resident_no_copy_counts_duplicates(sg, orc):
+    # benchmark mode without output copies: skipped frames still become duplicates once
+    # a frame was emitted (has-output flag independent of the payload copy)
+    D = 1024
+    frames = u8_stream("static", D, 2, 4)
+    cfg = sg.EngineConfig(n_steps=1, ssf_enabled=True, seed=3, d_latent=D)
+    want = orc.run_pipeline(make_cfg(n_steps=1, ssf_enabled=True, seed=3, d_latent=D),
+                            np.concatenate([frames] * 3).astype(np.float64))
+    p = sg.Pipeline(cfg, 1, D, ring_depth=4)
+    p.upload_resident(frames)
+    for _ in range(12):
+        p.push_resident(copy_outputs=False)
+    p.finish()
+    p.sync()
+    rep = p.report(0)
+    p.close()
+    for k in ("duplicates", "stale_skips", "frames_out", "ssf_skipped"):
+        assert rep[k] == want.report[k], (k, rep[k], want.report[k])

@@ -1,17 +1,17 @@
 """B200 analogues of the reference's bench tables (bench.cpp:225-285,
-engine.cpp:240-309) with the real UNet + TAESD pipeline, measured by bench.py:
+engine.cpp:213-309) with the real UNet + TAESD, all device-timed:
 
-  stream_batch    n-step denoising as Stream Batch (one n-row UNet call per tick)
-                  vs sequential (n one-row UNet calls per frame) vs wait-and-batch
-                  (n calls of an n-frame batch: same work as Stream Batch, latency 2n)
+  stream_batch    n-step denoising three ways, each MEASURED as one CUDA graph:
+                  Stream Batch (bench.py: the full pipeline, one n-row UNet call per
+                  tick), sequential (per frame: encode, n one-row UNet calls, decode;
+                  sdx_bench_denoise_loop(1, n, 1)) and wait-and-batch (per n frames:
+                  encode n, n calls of n rows, decode n; sdx_bench_denoise_loop(n, n, n)).
+                  The sequential / wait-and-batch graphs leave out the SSF gate and the
+                  fused step kernel (~0.03 ms per frame, see the stage times).
   guidance        frames/s and UNet rows per frame for none / cfg / self-negative /
                   onetime-negative (R-CFG) at n = 1 and 4
-  ssf             the similarity filter on a near-static vs a dynamic stream
-
-Each entry is one `python bench.py ...` run (device-timed, resident frames);
-sequential and wait-and-batch per-frame times are composed from the measured
-stage times (denoiser at 1 and n rows, codec, control), as the reference does
-from its cost model.
+  ssf             the similarity filter on a dynamic and a near-static scene, on and
+                  off, with the measured skip rate
 
     python tools/bench_tables.py [--out gpurun_out/bench_tables]
 """
@@ -33,27 +33,36 @@ def bench(*args):
     return json.loads(p.stdout.strip().splitlines()[-1])
 
 
+def denoise_loop(rows, calls, frames, n, iters=12):
+    import ctypes as C
+
+    sys.path.insert(0, ROOT)
+    from paper_2312_12491_b200 import _lib as L
+
+    f = L.lib.sdx_bench_denoise_loop
+    f.restype = C.c_int
+    f.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.POINTER(C.c_double)]
+    ms = C.c_double()
+    st = f(rows, calls, frames, n, iters, 0, 0, C.byref(ms))
+    if st != 0:
+        raise RuntimeError(L.lib.sdx_last_error())
+    return ms.value
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "bench_tables"))
     args = ap.parse_args()
     res = {"stream_batch": [], "guidance": [], "ssf": []}
-    one = bench("--n-steps", "1")
-    st1 = one["stage_ms_per_step"]
-    den1 = st1["denoiser"]
-    codec = st1["encode"] + st1["decode"]
-    other = st1["ssf"] + st1["control"] + st1["step"]
     for n in (1, 2, 4):
-        r = bench("--n-steps", str(n)) if n > 1 else one
-        st = r["stage_ms_per_step"]
+        r = bench("--n-steps", str(n))
         stream_ms = r["ms_per_step"]  # one output frame per step at steady state
-        seq_ms = n * den1 + codec + n * (other)
-        wab_ms = st["denoiser"] + codec + other  # n calls of n rows for n frames == per frame one n-row call
+        seq_ms = denoise_loop(1, n, 1, n)
+        wab_ms = denoise_loop(n, n, n, n) / n
         res["stream_batch"].append({"n": n, "sequential_ms": round(seq_ms, 3), "stream_ms": round(stream_ms, 3),
                                     "wait_and_batch_ms": round(wab_ms, 3), "speedup": round(seq_ms / stream_ms, 3),
                                     "stream_latency_ticks": n, "wait_and_batch_latency_ticks": 2 * n,
-                                    "unet_ms_n_rows": round(st["denoiser"], 3), "unet_ms_1_row": round(den1, 3),
-                                    "fps": r["value"]})
+                                    "unet_ms_n_rows": r["stage_ms_per_step"]["denoiser"], "fps": r["value"]})
     rows_per_frame = {"none": lambda n: n, "cfg": lambda n: 2 * n, "self_negative": lambda n: n,
                       "onetime_negative": lambda n: n + 1}
     for n in (1, 4):
@@ -66,15 +75,19 @@ def main():
         row["cfg_over_self"] = round(row["cfg_ms"] / row["self_negative_ms"], 3)
         row["cfg_over_onetime"] = round(row["cfg_ms"] / row["onetime_negative_ms"], 3)
         res["guidance"].append(row)
-    for label, extra in (("ssf on", []), ("ssf off", ["--no-ssf"])):
-        r = bench("--n-steps", "4", *extra)
-        res["ssf"].append({"config": label, "fps": r["value"], "ms_per_step": r["ms_per_step"],
-                           "denoiser_ms": r["stage_ms_per_step"]["denoiser"]})
+    for scene in ("dynamic", "near-static"):
+        for label, extra in (("on", []), ("off", ["--no-ssf"])):
+            r = bench("--n-steps", "4", "--scene", scene, *extra)
+            res["ssf"].append({"scene": scene, "ssf": label, "fps": r["value"], "ms_per_step": r["ms_per_step"],
+                               "skip_rate": r["config"]["ssf_skip_rate"],
+                               "denoiser_ms": r["stage_ms_per_step"]["denoiser"]})
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     json.dump(res, open(args.out + ".json", "w"), indent=1)
-    lines = ["# B200 bench tables (bench.py, 1 B200, UNet + TAESD 512x512, device-timed)", "",
+    lines = ["# B200 bench tables (1 B200, UNet + TAESD 512x512, every column device-timed)", "",
              "## stream_batch (bench.cpp:225-244, engine.cpp:240-309)", "",
-             "| n | sequential ms/frame | stream ms/frame | wait-and-batch ms/frame | speedup | latency stream / w&b (ticks) |",
+             "sequential and wait-and-batch: one CUDA graph of encode + UNet calls + decode "
+             "(sdx_bench_denoise_loop); stream: the full pipeline (bench.py)", "",
+             "| n | sequential ms/frame | stream ms/frame | wait-and-batch ms/frame | speedup vs sequential | latency stream / w&b (ticks) |",
              "|---|---|---|---|---|---|"]
     for r in res["stream_batch"]:
         lines.append(f"| {r['n']} | {r['sequential_ms']} | {r['stream_ms']} | {r['wait_and_batch_ms']} | {r['speedup']} | "
@@ -87,10 +100,11 @@ def main():
                      f"{r['cfg_over_self']} | {r['cfg_over_onetime']} | {r['none_unet_rows_per_frame']}, "
                      f"{r['cfg_unet_rows_per_frame']}, {r['self_negative_unet_rows_per_frame']}, "
                      f"{r['onetime_negative_unet_rows_per_frame']} |")
-    lines += ["", "## ssf (bench stream: moving gradients + noise, eta 0.98)", "", "| config | frames/s | ms/step |",
-              "|---|---|---|"]
+    lines += ["", "## ssf (eta 0.98, 4-step; the near-static scene redraws ~2% of the bytes per frame)", "",
+              "| scene | SSF | frames/s | ms/step | skip rate | UNet ms/step |", "|---|---|---|---|---|---|"]
     for r in res["ssf"]:
-        lines.append(f"| {r['config']} | {r['fps']} | {r['ms_per_step']} |")
+        lines.append(f"| {r['scene']} | {r['ssf']} | {r['fps']} | {r['ms_per_step']} | {r['skip_rate']} | "
+                     f"{r['denoiser_ms']} |")
     open(args.out + ".md", "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
