@@ -70,6 +70,9 @@ int sdx_kernel_gemm_debug(void* dbg);
 int sdx_kernel_gemm_probe(int mode);
 /* Same for the attention kernel: 1 = no MMAs, 2 = no softmax exponentials. */
 int sdx_kernel_attention_probe(int mode);
+/* Device buffer of [10 warps][64 KV blocks][8] clock64 phase stamps of CTA 0 of the next
+ * attention launches (NULL disables); see attention_sm100.cu. */
+int sdx_kernel_attention_debug(void* dbg);
 
 /* The batched UNet denoiser (random-init SD-2.1/SD-turbo topology, bf16
  * weights, fp32 accumulation) used by the pipeline's predict_eps_batch slot.

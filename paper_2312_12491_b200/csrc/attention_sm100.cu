@@ -41,8 +41,15 @@ constexpr int KVS = PB == 2 ? 2 : 4;  // K/V ring depth
 // (190.7 vs 190.2 us, tools/attn_probe.py): the softmax warps, not the MMA order, set
 // the pace.
 constexpr int kSAhead = 1;
-constexpr int KVS_TS = 6;  // K/V ring of the TMEM-P kernel (no P buffers in smem)
+constexpr int KVS_TS = 5;
+constexpr bool kStaggerTiles = true;
+// attn_ts_kernel<POLY>: one exp2 pair in POLY (pairs 1, 1 + POLY, ...) on the FMA-pipe
+// polynomial, 0 = all on the MUFU; SDX_ATTN_POLY picks the instantiation (default kPolyDefault)
+constexpr int kPolyDefault = 3;  // K/V ring of the TMEM-P kernel (no P buffers in smem)
 
+// Blocking wait with a suspend-time hint: the warp sleeps in the barrier unit instead of
+// re-polling, so waiting warps leave the issue slots of their SM sub-partition to the
+// softmax warps sharing it (the slowest of a tile's four softmax warps sets its pace).
 __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
     const uint32_t a = smem_u32(bar);
     uint32_t done = 0;
@@ -50,7 +57,7 @@ __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t phase) {
     while (true) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 1000000;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
             : "r"(a), "r"(phase)
@@ -367,14 +374,37 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // ---- P in TMEM (FA4-style TS-MMA) -------------------------------------------------------
-// tcgen05.mma with the A operand in tensor memory: D[tmem] (+)= A[tmem] * B[smem]
-__device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                           uint32_t accumulate) {
+// The MMA warp runs converged and one lane, elected inside the asm, issues each
+// tcgen05 op: with warp-uniform operands ptxas emits a plain UTCHMMA instead of an
+// ELECT / R2UR.BROADCAST loop around it, which costs ~50 cycles per MMA
+// (tools/ubench/ubench_mma.cu: an M128 N64 TS-MMA issues every 51 cycles from a
+// divergent lane, every 32 = the tensor-pipe floor from the converged warp).
+__device__ __forceinline__ void umma_ss_el(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]
+__device__ __forceinline__ void umma_ts_el(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit_el(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
         : "memory");
 }
 
@@ -415,15 +445,49 @@ __device__ __forceinline__ void fadd2_acc(float& d0, float& d1, float a0, float 
         : "f"(a0), "f"(a1));
 }
 
-// Two 128-query tiles per CTA, as attn_kernel, with the FA4 data flow: the softmax
-// warps read S_t(j) from TMEM, write P_t(j) = exp2(...) as packed bf16 back into the
-// first 64 columns of the same TMEM region (tcgen05.st), and PV_t(j) reads P straight
-// from TMEM as the A operand (TS-MMA).  No P in shared memory, no proxy fence, no
-// wait for PV(j-1) before the exponentials.  The MMA warp issues, per tile, PV_t(j)
-// and then S_t(j+1) into the same columns (MMAs execute in issue order), so the
-// commit that releases S_t(j+1) to the softmax also certifies O_t through block j.
-// TMEM: S/P of tile t at columns 128 t, O of tile t at 256 + 64 t.
-__global__ void __launch_bounds__(320, 1)
+// exp2 of a pair on the FMA pipe (FA4's emulation): 2^x = 2^round(x) * 2^f, f in [-0.5, 0.5],
+// 2^f by a degree-3 polynomial (relative error 7.7e-5, below the bf16 rounding of P), the
+// integer part added to the exponent bits.  round(x) comes from the 1.5 * 2^23 trick, whose
+// low mantissa bits hold it.  x is clamped at -126 (exp2(-inf) for masked keys -> ~1e-38).
+__device__ __forceinline__ void ex2_poly2(float& p0, float& p1, float x0, float x1) {
+    x0 = fmaxf(x0, -126.f);
+    x1 = fmaxf(x1, -126.f);
+    uint32_t t0, t1;
+    asm("{\n\t.reg .b64 vx, vm, vt, vxi, vf, vp, vc3, vc2, vc1, vc0;\n\t"
+        "mov.b64 vx, {%4, %5};\n\t"
+        "mov.b64 vm, {%6, %6};\n\t"
+        "add.rn.ftz.f32x2 vt, vx, vm;\n\t"
+        "sub.rn.ftz.f32x2 vxi, vt, vm;\n\t"
+        "sub.rn.ftz.f32x2 vf, vx, vxi;\n\t"
+        "mov.b64 vc3, {%7, %7};\n\t"
+        "mov.b64 vc2, {%8, %8};\n\t"
+        "mov.b64 vc1, {%9, %9};\n\t"
+        "mov.b64 vc0, {%10, %10};\n\t"
+        "fma.rn.ftz.f32x2 vp, vf, vc3, vc2;\n\t"
+        "fma.rn.ftz.f32x2 vp, vp, vf, vc1;\n\t"
+        "fma.rn.ftz.f32x2 vp, vp, vf, vc0;\n\t"
+        "mov.b64 {%0, %1}, vp;\n\t"
+        "mov.b64 {%2, %3}, vt;\n\t}"
+        : "=f"(p0), "=f"(p1), "=r"(t0), "=r"(t1)
+        : "f"(x0), "f"(x1), "f"(12582912.f), "f"(0.05508877f), "f"(0.24260466f), "f"(0.69327628f), "f"(0.9999289f));
+    p0 = __uint_as_float(__float_as_uint(p0) + (t0 << 23));
+    p1 = __uint_as_float(__float_as_uint(p1) + (t1 << 23));
+}
+
+// Two 128-query tiles per CTA, as attn_kernel, with P in tensor memory.  Per tile t:
+// S_t (fp32, 128 columns), O_t (64), P_t (bf16 pairs, 64) are TMEM-resident, so
+//   * S_t(j+1) = Q_t K(j+1)^T is issued as soon as the softmax has read S_t(j) into
+//     registers (s_free) and overlaps the exponentials of block j;
+//   * the softmax writes P_t(j) with tcgen05.st and PV_t(j) reads it as the A operand
+//     (TS-MMA): no P in shared memory, no proxy fence; the only wait before writing
+//     P_t(j) is PV_t(j-1) having read P_t(j-1) (pv_done), long done by then.
+// Q and K/V come in by TMA (S = Q K^T is an SS-MMA: M128 N128 runs at the tensor-pipe
+// floor).  TMEM: S_t at 128 t, O_t at 256 + 64 t, P_t at 384 + 64 t.
+// 11 warps: 0 TMA, 1 + t the MMA issuer of tile t (a tcgen05.mma issue blocks about as
+// long as the MMA runs, so one issuer per tile keeps one tile's S(j+1) from queueing
+// behind the other tile's PV), 3..6 softmax of tile 0, 7..10 softmax of tile 1.
+template <int POLY>
+__global__ void __launch_bounds__(352, 1)
     attn_ts_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv, AttnArgs a) {
     const int npairs = (a.q_len + 2 * BQ - 1) / (2 * BQ);
     const bool single = static_cast<int>(blockIdx.x) >= a.pair_base;
@@ -445,10 +509,11 @@ __global__ void __launch_bounds__(320, 1)
     uint64_t* q_full = bars + 0;
     uint64_t* kv_full = bars + 1;            // [KVS_TS]
     uint64_t* kv_empty = kv_full + KVS_TS;   // [KVS_TS]
-    uint64_t* s_full = kv_empty + KVS_TS;    // [2] S_t(j) in TMEM (and O_t final through j-1)
-    uint64_t* p_full = s_full + 2;           // [2] P_t(j) in TMEM
-    uint64_t* o_full = p_full + 2;           // [2] O_t final
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+    uint64_t* s_full = kv_empty + KVS_TS;    // [2] S_t(j) in TMEM
+    uint64_t* s_free = s_full + 2;           // [2] S_t(j) read by the softmax (S_t(j+1) may overwrite)
+    uint64_t* p_full = s_free + 2;           // [2] P_t(j) in TMEM
+    uint64_t* pv_done = p_full + 2;          // [2] PV_t(j) complete (P_t free, O_t final through j)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkv = (a.kv_len + BKV - 1) / BKV;
@@ -462,12 +527,13 @@ __global__ void __launch_bounds__(320, 1)
         mbar_init(q_full, 1);
         for (int i = 0; i < KVS_TS; ++i) {
             mbar_init(&kv_full[i], 1);
-            mbar_init(&kv_empty[i], 1);
+            mbar_init(&kv_empty[i], has1 ? 2 : 1);  // released by each tile's MMA issuer
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&p_full[i], 4);  // one arrival per softmax warp
-            mbar_init(&o_full[i], 1);
+            mbar_init(&s_free[i], 4);  // one arrival per softmax warp
+            mbar_init(&p_full[i], 4);
+            mbar_init(&pv_done[i], 1);
         }
         fence_barrier_init();
     }
@@ -478,6 +544,8 @@ __global__ void __launch_bounds__(320, 1)
     const uint32_t tmem = *tmem_slot;
     pdl_wait();
     const bool live = !(a.rows_dev && img >= *a.rows_dev);
+    long long* dbg = (a.dbg && blockIdx.x == 0 && lane == 0) ? a.dbg + warp * 64 * 8 : nullptr;
+    if (dbg && warp == 0) a.dbg[7] = clock64();
 
     if (!live) {
     } else if (warp == 0) {
@@ -493,72 +561,61 @@ __global__ void __launch_bounds__(320, 1)
                 tma_load_2d(sV + b * TILE_BYTES, &tkv, &kv_full[b], a.v_col0 + head * HD, kv_row0 + j * BKV);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {
+    } else if (warp == 1 || warp == 2) {
+        // MMA issuer of tile t: converged warp, every issue / commit through one elected lane
+        const int t = warp - 1;
+        if (t == 0 || has1) {
             constexpr uint32_t idesc_s = idesc_bf16(128, 128);
             constexpr uint32_t idesc_o = idesc_bf16(128, 64, 0, 1);  // B (= V) MN-major
-            const int ntile = has1 ? 2 : 1;
-            auto issue_s = [&](int t, int j) {
-                const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ + t * TILE_BYTES));
+            const uint64_t dq = desc_kmajor_sw128(smem_u32(sQ + t * TILE_BYTES));
+            auto issue_s = [&](int j) {
                 const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + (j % KVS_TS) * TILE_BYTES));
 #pragma unroll
-                for (int k = 0; k < HD / 16; ++k) umma_f16(tmem + t * 128, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
-                umma_commit(&s_full[t]);
-            };
-            auto issue_pv = [&](int t, int j) {
-                const uint32_t vbase = smem_u32(sV + (j % KVS_TS) * TILE_BYTES);
-#pragma unroll
-                for (int k = 0; k < BKV / 16; ++k)  // P: 16 keys = 8 packed columns per MMA
-                    umma_f16_ts(tmem + 256 + t * 64, tmem + t * 128 + 8 * k, desc_mnmajor_sw128(vbase + k * 2048, 0),
-                                idesc_o, (j > 0 || k != 0) ? 1u : 0u);
+                for (int k = 0; k < HD / 16; ++k) umma_ss_el(tmem + t * 128, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
+                umma_commit_el(&s_full[t]);
             };
             wait_bar(q_full, 0);
             wait_bar(&kv_full[0], 0);
             tc_fence_after();
-            for (int t = 0; t < ntile; ++t) issue_s(t, 0);
-            int np[2] = {0, ntile > 1 ? 0 : nkv};  // next PV block per tile
-            int released = 0;
-            const long long t0 = clock64();
-            while (released < nkv) {
-                bool progress = false;
+            issue_s(0);
+            for (int j = 0; j < nkv; ++j) {
+                if (j + 1 < nkv) {
+                    // S_t(j+1) once the softmax holds S_t(j) in registers and K(j+1) has landed
+                    wait_bar(&s_free[t], j & 1);
+                    wait_bar(&kv_full[(j + 1) % KVS_TS], ((j + 1) / KVS_TS) & 1);
+                    tc_fence_after();
+                    issue_s(j + 1);
+                    if (dbg && j < 64) dbg[j * 8 + 1] = clock64();
+                }
+                wait_bar(&p_full[t], j & 1);
+                if (dbg && j < 64) dbg[j * 8 + 0] = clock64();
+                tc_fence_after();
+                const uint32_t vbase = smem_u32(sV + (j % KVS_TS) * TILE_BYTES);
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    if (np[t] < nkv && mbar_test(&p_full[t], np[t] & 1)) {
-                        tc_fence_after();
-                        issue_pv(t, np[t]);
-                        const int j1 = np[t] + 1;
-                        if (j1 < nkv) {
-                            wait_bar(&kv_full[j1 % KVS_TS], (j1 / KVS_TS) & 1);
-                            tc_fence_after();
-                            issue_s(t, j1);  // overwrites P_t(j): issued after PV_t(j), executed in order
-                        } else {
-                            umma_commit(&o_full[t]);
-                        }
-                        np[t] = j1;
-                        progress = true;
-                    }
-                }
-                const int done = np[0] < np[1] ? np[0] : np[1];
-                while (released < done) umma_commit(&kv_empty[released++ % KVS_TS]);
-                if (!progress && clock64() - t0 > (1LL << 34)) {
-                    printf("sdx attention(ts): MMA issue watchdog (block %d)\n", blockIdx.x);
-                    asm volatile("trap;");
-                }
+                for (int k = 0; k < BKV / 16; ++k)  // P: 16 keys = 8 packed columns per MMA
+                    umma_ts_el(tmem + 256 + t * 64, tmem + 384 + t * 64 + 8 * k,
+                               desc_mnmajor_sw128(vbase + k * 2048, 0), idesc_o, (j > 0 || k != 0) ? 1u : 0u);
+                umma_commit_el(&pv_done[t]);
+                umma_commit_el(&kv_empty[j % KVS_TS]);
+                if (dbg && j < 64) dbg[j * 8 + 2] = clock64();
             }
         }
-        __syncwarp();
     } else {
-        const int t = (warp - 2) >> 2;  // q tile of this softmax warpgroup
+        const int t = (warp - 3) >> 2;  // q tile of this softmax warpgroup
         const int q = warp & 3;         // TMEM lane quarter this warp may access
         const int r = q * 32 + lane;
         if (t == 0 || has1) {
             const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
             const uint32_t s_addr = tmem + lane_off + t * 128;
             const uint32_t o_addr = tmem + lane_off + 256 + t * 64;
+            const uint32_t p_addr = tmem + lane_off + 384 + t * 64;
             const float sl2 = a.scale * 1.4426950408889634f;
             float m_used = -INFINITY, l0 = 0.f, l1 = 0.f;
             for (int j = 0; j < nkv; ++j) {
+                long long* dj = (dbg && j < 64) ? dbg + j * 8 : nullptr;
+                if (dj) dj[0] = clock64();
                 wait_bar(&s_full[t], j & 1);
+                if (dj) dj[1] = clock64();
                 tc_fence_after();
                 uint32_t sr[128];
                 tmem_ld32_nowait(s_addr + 0, sr);
@@ -569,6 +626,11 @@ __global__ void __launch_bounds__(320, 1)
                 tmem_wait_ld32(sr + 32);
                 tmem_wait_ld32(sr + 64);
                 tmem_wait_ld32(sr + 96);
+                // S_t(j) is in registers: S_t(j+1) may overwrite the TMEM columns
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s_free[t]);
+                if (dj) dj[2] = clock64();
                 const int kv_valid = a.kv_len - j * BKV;
                 if (kv_valid < BKV) {  // partial last block: masked keys read as -inf
 #pragma unroll
@@ -586,13 +648,15 @@ __global__ void __launch_bounds__(320, 1)
                         mx4[k] = fmax3f(mx4[k], __uint_as_float(sr[i + k]), __uint_as_float(sr[i + 4 + k]));
                 }
                 const float m_row = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * sl2;
+                // PV_t(j-1) done: P_t is free and O_t final through block j-1
+                if (j > 0) wait_bar(&pv_done[t], (j - 1) & 1);
+                tc_fence_after();
                 // lazy rescale (warp-uniform: the TMEM accesses are warp-collective): move the
                 // reference max only when some row's max grew by more than 2^8
                 if (__any_sync(0xffffffffu, m_row > m_used + 8.f)) {
                     const float m_new = fmaxf(m_used, m_row);
                     const float corr = ex2(m_used - m_new);  // m_used = -inf -> 0
                     if (j > 0) {
-                        // O_t is final through block j-1: s_full(j) was committed after PV_t(j-1)
 #pragma unroll
                         for (int c = 0; c < HD; c += 16) {
                             float v[16];
@@ -606,6 +670,11 @@ __global__ void __launch_bounds__(320, 1)
                     l1 *= corr;
                     m_used = m_new;
                 }
+                // stagger the tiles once: tile 1 starts its first exponentials when tile 0 has
+                // finished its own, so one tile's exponentials overlap the other's S load,
+                // max and PV wait instead of both tiles contending for the MUFU at once
+                if (t == 1 && j == 0 && kStaggerTiles) wait_bar(&p_full[0], 0);
+                if (dj) dj[3] = clock64();
                 // P = exp2(s * scale_log2 - m_used) as packed bf16 into TMEM (exp2(-inf) = 0)
                 const float nm = -m_used;
 #pragma unroll
@@ -613,20 +682,26 @@ __global__ void __launch_bounds__(320, 1)
                     uint32_t pk[16];
 #pragma unroll
                     for (int i = 0; i < 32; i += 2) {
-                        float x0, x1;
+                        float x0, x1, p0, p1;
                         ffma2_bc(x0, x1, __uint_as_float(sr[c + i]), __uint_as_float(sr[c + i + 1]), sl2, nm);
-                        const float p0 = ex2(x0), p1 = ex2(x1);
+                        if (POLY > 0 && (i / 2) % POLY == 1) {
+                            ex2_poly2(p0, p1, x0, x1);  // FMA pipe: unloads the MUFU (16 ex2 / clk / SM)
+                        } else {
+                            p0 = ex2(x0);
+                            p1 = ex2(x1);
+                        }
                         fadd2_acc(l0, l1, p0, p1);
                         pk[i / 2] = pack_bf16(p0, p1);
                     }
-                    tmem_st16u(s_addr + (c >> 1), pk);
+                    tmem_st16u(p_addr + (c >> 1), pk);
                 }
                 tmem_wait_st();
+                if (dj) dj[4] = clock64();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&p_full[t]);
             }
-            wait_bar(&o_full[t], 0);
+            wait_bar(&pv_done[t], (nkv - 1) & 1);
             tc_fence_after();
             const int qi = q_first + t * BQ + r;
             float o[HD];
@@ -690,6 +765,9 @@ AttnPlan plan_attention(const __nv_bfloat16* q, long long q_rows_total, long lon
     encode_rows(&p.tq, q, q_rows_total, ld_q, ld_q);
     encode_rows(&p.tkv, kv, kv_rows_total, ld_kv, ld_kv);
     p.a.q_col0 = q_col0;
+    p.a.q = q;
+    p.a.q_rows_total = q_rows_total;
+    p.a.ld_q = ld_q;
     p.a.k_col0 = k_col0;
     p.a.v_col0 = v_col0;
     p.a.out = out;
@@ -710,8 +788,10 @@ AttnPlan plan_attention(const __nv_bfloat16* q, long long q_rows_total, long lon
 
 namespace {
 int g_attn_xmode = 0;
+long long* g_attn_dbg = nullptr;
 }
 void set_attention_probe_mode(int mode) { g_attn_xmode = mode; }
+void set_attention_debug_buffer(long long* dbg) { g_attn_dbg = dbg; }
 
 // SDX_ATTN_TS=0: the P-in-shared-memory kernel (attn_kernel) instead of attn_ts_kernel
 static bool attn_ts_enabled() {
@@ -722,13 +802,25 @@ static bool attn_ts_enabled() {
     return on;
 }
 
+static int attn_poly() {
+    static const int v = [] {
+        const char* e = std::getenv("SDX_ATTN_POLY");
+        return e ? std::atoi(e) : kPolyDefault;
+    }();
+    return v;
+}
+
 void run_attention(const AttnPlan& p, cudaStream_t st) {
     const bool ts = attn_ts_enabled() && g_attn_xmode == 0;
+    const int poly = attn_poly();
+    auto ts_kern = poly == 2 ? attn_ts_kernel<2> : poly == 3 ? attn_ts_kernel<3> : poly == 4 ? attn_ts_kernel<4>
+                 : poly == 6 ? attn_ts_kernel<6> : attn_ts_kernel<0>;
     const size_t smem = ts ? (2 + 2 * KVS_TS) * TILE_BYTES + 1024 + 256 : (2 + 2 * KVS + 4 * PB) * TILE_BYTES + 1024 + 256;
-    if (ts) ensure_kernel_attrs(attn_ts_kernel, smem);
+    if (ts) ensure_kernel_attrs(ts_kern, smem);
     else ensure_kernel_attrs(attn_kernel, smem);
     AttnArgs a = p.a;
     a.xmode = g_attn_xmode;
+    a.dbg = g_attn_dbg;
     a.heads = p.heads;
     const int npairs = (p.a.q_len + 2 * BQ - 1) / (2 * BQ);
     const int total = npairs * p.heads * p.images;
@@ -741,7 +833,8 @@ void run_attention(const AttnPlan& p, cudaStream_t st) {
     a.single = 0;
     a.unit_base = 0;
     a.pair_base = full;
-    launch_pdl(ts ? attn_ts_kernel : attn_kernel, dim3(full + 2 * (total - full)), dim3(320), smem, st, p.tq, p.tkv, a);
+    launch_pdl(ts ? ts_kern : attn_kernel, dim3(full + 2 * (total - full)), dim3(ts ? 352 : 320), smem, st, p.tq,
+               p.tkv, a);
 }
 
 }  // namespace sdx

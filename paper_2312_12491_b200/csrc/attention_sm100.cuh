@@ -20,10 +20,15 @@ struct AttnArgs {
     int xmode;                    // experiments only: 1 = no MMAs, 2 = no softmax math (pipeline probes)
     int heads;                    // set by run_attention
     int single, unit_base, pair_base;  // CTAs >= pair_base run single-tile units (the tail); single/unit_base unused
+    long long* dbg;               // experiments only: clock64 phase stamps of CTA 0 (null = off)
+    const __nv_bfloat16* q;       // Q rows for the TMEM-resident A operand (attn_ts_kernel)
+    long long q_rows_total, ld_q;
 };
 
 // Pipeline probe for kernel experiments (results wrong): 0 off, 1 no MMAs, 2 no softmax math.
 void set_attention_probe_mode(int mode);
+// Experiments: device buffer of [10 warps][64 blocks][8] clock64 stamps for CTA 0 (null = off).
+void set_attention_debug_buffer(long long* dbg);
 
 struct AttnPlan {
     CUtensorMap tq, tkv;

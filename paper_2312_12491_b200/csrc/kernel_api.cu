@@ -201,6 +201,9 @@ int sdx_kernel_gemm_probe(int mode) {
 int sdx_kernel_attention_probe(int mode) {
     return kguard([&] { sdx::set_attention_probe_mode(mode); });
 }
+int sdx_kernel_attention_debug(void* dbg) {
+    return kguard([&] { sdx::set_attention_debug_buffer(static_cast<long long*>(dbg)); });
+}
 
 int sdx_kernel_plan_destroy(sdx_gemm_plan* p) {
     return kguard([&] { delete p; });
