@@ -379,35 +379,6 @@ __global__ void __launch_bounds__(320, 1)
 // ELECT / R2UR.BROADCAST loop around it, which costs ~50 cycles per MMA
 // (tools/ubench/ubench_mma.cu: an M128 N64 TS-MMA issues every 51 cycles from a
 // divergent lane, every 32 = the tensor-pipe floor from the converged warp).
-__device__ __forceinline__ void umma_ss_el(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// D[tmem] (+)= A[tmem] * B[smem]
-__device__ __forceinline__ void umma_ts_el(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p, e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void umma_commit_el(uint64_t* bar) {
-    asm volatile(
-        "{\n\t.reg .pred e;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
-        : "memory");
-}
-
 __device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t* v) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -571,7 +542,7 @@ __global__ void __launch_bounds__(352, 1)
             auto issue_s = [&](int j) {
                 const uint64_t dk = desc_kmajor_sw128(smem_u32(sK + (j % KVS_TS) * TILE_BYTES));
 #pragma unroll
-                for (int k = 0; k < HD / 16; ++k) umma_ss_el(tmem + t * 128, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
+                for (int k = 0; k < HD / 16; ++k) umma_f16_el(tmem + t * 128, dq + 2 * k, dk + 2 * k, idesc_s, k != 0);
                 umma_commit_el(&s_full[t]);
             };
             wait_bar(q_full, 0);

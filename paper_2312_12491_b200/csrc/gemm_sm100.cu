@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
             }
         }
     } else if (HALO && warp == 1) {
-        if (lane == 0) {
+        {  // converged warp, elected-lane issue (sm100.cuh)
             constexpr uint32_t idesc = idesc_bf16(BM, BN);
             wait_bounded(bfull, 0);
             uint32_t it = 0;
@@ -265,10 +265,10 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                     const uint64_t db = desc_kmajor_sw128(smem_u32(sB + tap * B_BYTES));
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        umma_f16(dtm, da + 2 * k, db + 2 * k, idesc, (tap != 0 || k != 0) ? 1u : 0u);
+                        umma_f16_el(dtm, da + 2 * k, db + 2 * k, idesc, (tap != 0 || k != 0) ? 1u : 0u);
                 }
-                umma_commit(&empty[s]);
-                umma_commit(&tfull[acc]);
+                umma_commit_el(&empty[s]);
+                umma_commit_el(&tfull[acc]);
             }
         }
         __syncwarp();
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && rank == 0) {  // CTA pair: only the leader issues the 2-SM MMAs
+        if (rank == 0) {  // converged warp, elected-lane issue; CTA pair: only the leader issues
             constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN);
             uint32_t it = 0, lt = 0;
             for (int u = ustart; u < total; u += ustep, ++lt) {
@@ -352,21 +352,21 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                     const int s = it % STAGES;
                     const uint32_t ph = (it / STAGES) & 1;
                     wait_bounded(&full[s], ph);
-                    if (dbg && it == 0) dbg[2] = gtimer();
+                    if (dbg && it == 0 && lane == 0) dbg[2] = gtimer();
                     tc_fence_after();
                     const uint64_t da = desc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
                     const uint64_t db = desc_kmajor_sw128(smem_u32(sB + s * B_BYTES));
 #pragma unroll
                     for (int k = 0; k < (g.xmode == 1 ? 0 : BK / 16); ++k) {  // +32 B per K=16 step in the swizzle atom
-                        if (PAIR) umma_f16_pair(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-                        else umma_f16(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                        if (PAIR) umma_f16_pair_el(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                        else umma_f16_el(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                     }
-                    if (PAIR) umma_commit_pair(&empty[s], 3);
-                    else umma_commit(&empty[s]);
+                    if (PAIR) umma_commit_pair_el(&empty[s], 3);
+                    else umma_commit_el(&empty[s]);
                 }
-                if (PAIR) umma_commit_pair(&tfull[acc], 3);
-                else umma_commit(&tfull[acc]);
-                if (dbg && lt == 0) dbg[3] = gtimer();
+                if (PAIR) umma_commit_pair_el(&tfull[acc], 3);
+                else umma_commit_el(&tfull[acc]);
+                if (dbg && lt == 0 && lane == 0) dbg[3] = gtimer();
             }
         }
         __syncwarp();
