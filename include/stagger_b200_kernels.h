@@ -87,6 +87,9 @@ int sdx_unet_forward(sdx_unet* u, const float* x, int rows, const int* row_step,
 int sdx_unet_param_count(sdx_unet* u, int* n);
 int sdx_unet_param(sdx_unet* u, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32);
 int sdx_unet_flops_per_row(sdx_unet* u, double* flops);
+// Device ms per whole forward at `rows` rows: the forward as one CUDA graph replayed `iters`
+// times back to back (tools only).
+int sdx_unet_time_forward(sdx_unet* u, int rows, int iters, float* ms_per_forward);
 int sdx_unet_profile(sdx_unet* u, int rows, int cap, const char** kinds, float* ms, int* count);
 int sdx_unet_profile_detail(sdx_unet* u, int rows, int cap, const char** labels, double* flops, float* ms,
                             int* count);

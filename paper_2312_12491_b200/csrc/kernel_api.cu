@@ -348,6 +348,48 @@ int sdx_unet_forward(sdx_unet* u, const float* x, int rows, const int* row_step,
     });
 }
 
+// Device time of whole forwards at `rows` rows: one forward captured in a CUDA graph,
+// replayed `iters` times back to back (weights stream from HBM every forward, as in
+// the pipeline: 1.7 GB of them do not stay in the 126 MB L2), CUDA events around
+// the replays.  Kernel benchmarks / tools only.
+int sdx_unet_time_forward(sdx_unet* u, int rows, int iters, float* ms_per_forward) {
+    return kguard([&] {
+        auto* n = u->net;
+        if (rows < 1 || rows > n->config().rmax || iters < 1) sdx::raise(SDX_INVALID_ARGUMENT, "unet: bad rows/iters");
+        cudaStream_t st;
+        SDX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        int* d_rows = nullptr;
+        SDX_CUDA(cudaMalloc(&d_rows, sizeof(int)));
+        SDX_CUDA(cudaMemcpy(d_rows, &rows, sizeof(int), cudaMemcpyHostToDevice));
+        n->forward(d_rows, st);  // warm-up outside the graph
+        SDX_CUDA(cudaStreamSynchronize(st));
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        SDX_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        n->forward(d_rows, st);
+        SDX_CUDA(cudaStreamEndCapture(st, &g));
+        SDX_CUDA(cudaGraphInstantiate(&ge, g, 0));
+        SDX_CUDA(cudaGraphLaunch(ge, st));
+        SDX_CUDA(cudaStreamSynchronize(st));
+        cudaEvent_t e0, e1;
+        SDX_CUDA(cudaEventCreate(&e0));
+        SDX_CUDA(cudaEventCreate(&e1));
+        SDX_CUDA(cudaEventRecord(e0, st));
+        for (int i = 0; i < iters; ++i) SDX_CUDA(cudaGraphLaunch(ge, st));
+        SDX_CUDA(cudaEventRecord(e1, st));
+        SDX_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        SDX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        *ms_per_forward = ms / static_cast<float>(iters);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        cudaFree(d_rows);
+        cudaStreamDestroy(st);
+    });
+}
+
 int sdx_unet_param_count(sdx_unet* u, int* n) {
     return kguard([&] { *n = static_cast<int>(u->net->params().size()); });
 }

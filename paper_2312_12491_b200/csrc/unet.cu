@@ -110,7 +110,7 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
         float* b = wf32(nm + ".norm1.b", {Cin}, 0.f, 0.f);
         GnPlan gp = groupnorm(x, Cx, skip, Cs, HW, 1e-5f, g, b, 1, t1);
         gns_.push_back(gp);
-        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }, "groupnorm HW=" + std::to_string(HW) + " C=" + std::to_string(Cin) + (gp.cluster ? " cluster" : " split")});
     }
     // conv1 + bias + temb[row_step]
     bf16* h1 = act(M * Cout);
@@ -138,7 +138,7 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
         float* b = wf32(nm + ".norm2.b", {Cout}, 0.f, 0.f);
         GnPlan gp = groupnorm(h1, Cout, nullptr, 0, HW, 1e-5f, g, b, 1, t2);
         gns_.push_back(gp);
-        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }, "groupnorm HW=" + std::to_string(HW) + " C=" + std::to_string(Cout) + (gp.cluster ? " cluster" : " split")});
     }
     const bf16* shortcut = x;
     if (Cin != Cout || skip) {
@@ -245,7 +245,8 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
         }
         bf16* n = act(M * C);
         const int Mi = static_cast<int>(M);
-        ops_.push_back(Op{"layernorm", [=](cudaStream_t st) { run_layernorm(in, Mi, C, lg, lb, 1e-5f, n, rows, HW, st); }});
+        ops_.push_back(Op{"layernorm", [=](cudaStream_t st) { run_layernorm(in, Mi, C, lg, lb, 1e-5f, n, rows, HW, st); },
+                          "layernorm M=" + std::to_string(Mi) + " C=" + std::to_string(C)});
         gemm_op(kind, plan_gemm(n, C, w, C, static_cast<int>(M), N, C, e));
     };
     auto ln_params = [&](const std::string& n2, float** g, float** b) {
@@ -258,7 +259,7 @@ bf16* UNet::transformer(const bf16* x, int C, int H, int W, const std::string& n
         float* b = wf32(nm + ".norm.b", {C}, 0.f, 0.f);
         GnPlan gp = groupnorm(x, C, nullptr, 0, HW, 1e-6f, g, b, 0, t);
         gns_.push_back(gp);
-        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }});
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t st) { run_groupnorm(gp, st); }, "groupnorm HW=" + std::to_string(HW) + " C=" + std::to_string(C) + (gp.cluster ? " cluster" : " split")});
     }
     bf16* h = act(M * C);
     gemm("linear", t, C, wbf(nm + ".proj_in.w", {C, C}, wstd), C, wf32(nm + ".proj_in.b", {C}, 0.02f, 0.f), nullptr, h);
@@ -478,7 +479,7 @@ UNet::UNet(const UNetConfig& cfg, cudaStream_t st) : cfg_(cfg) {
         float* b = wf32("norm_out.b", {cur}, 0.f, 0.f);
         GnPlan gp = groupnorm(h, cur, nullptr, 0, H * W, 1e-5f, g, b, 1, t);
         gns_.push_back(gp);
-        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t s) { run_groupnorm(gp, s); }});
+        ops_.push_back(Op{"groupnorm", [gp](cudaStream_t s) { run_groupnorm(gp, s); }, "groupnorm HW=" + std::to_string(H * W) + " C=" + std::to_string(cur) + (gp.cluster ? " cluster" : " split")});
     }
     {
         GemmEpilogue e;

@@ -68,7 +68,7 @@ def sweep(label, make, flops, N, K, M=0, res=False):
     L.sdx_kernel_plan_destroy(h)
     best = (tm, mbn, ms)
     RECORDS.append({"label": label, "M": M, "N": N, "K": K, "res": res, "bn": mbn, "s": ms, "us": tm, "model": True})
-    for bn in BNS:
+    for bn in ([] if os.environ.get("SDX_SWEEP_MODEL_ONLY") else BNS):
         if N <= 64 and abs(bn) > 64:
             continue
         for s in SPLITS:

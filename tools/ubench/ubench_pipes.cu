@@ -24,6 +24,16 @@ __global__ void pipe_kernel(float* out, long long* cyc, int iters) {
                 }
             }
             if (MODE == 3) v[i] = fmaf(v[i], 0.999f, 0.001f);
+            if (MODE == 4) {  // packed bf16x2 ex2: two exponentials per lane per instruction
+                uint32_t x = __float_as_uint(v[i]);
+                asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(x));
+                v[i] = __uint_as_float(x);
+            }
+            if (MODE == 5) {  // packed f16x2 ex2
+                uint32_t x = __float_as_uint(v[i]);
+                asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(x));
+                v[i] = __uint_as_float(x);
+            }
         }
     }
     const long long t1 = clock64();
@@ -37,10 +47,12 @@ int main() {
     cudaMalloc(&out, 148 * 8 * 1024 * sizeof(float));
     cudaMalloc(&cyc, 148 * 8 * sizeof(long long));
     const int iters = 4096;
-    const char* names[] = {"ex2+fmul (1 MUFU + 1 FMUL per elem)", "ex2 chain", "ffma2 (per pair)", "ffma"};
-    for (int mode = 0; mode < 4; ++mode) {
+    const char* names[] = {"ex2+fmul (1 MUFU + 1 FMUL per elem)", "ex2 chain", "ffma2 (per pair)", "ffma",
+                           "ex2.bf16x2 (per pair)", "ex2.f16x2 (per pair)"};
+    for (int mode = 0; mode < 6; ++mode) {
         for (int warps : {4, 8, 16}) {
-            auto k = mode == 0 ? pipe_kernel<0> : mode == 1 ? pipe_kernel<1> : mode == 2 ? pipe_kernel<2> : pipe_kernel<3>;
+            auto k = mode == 0 ? pipe_kernel<0> : mode == 1 ? pipe_kernel<1> : mode == 2 ? pipe_kernel<2> : mode == 3 ? pipe_kernel<3>
+                   : mode == 4 ? pipe_kernel<4> : pipe_kernel<5>;
             k<<<148, warps * 32>>>(out, cyc, iters);
             cudaDeviceSynchronize();
             k<<<148, warps * 32>>>(out, cyc, iters);
