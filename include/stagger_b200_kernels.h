@@ -104,6 +104,10 @@ int sdx_taesd_create(int imax, uint64_t seed, int device, sdx_taesd** out);
 int sdx_taesd_destroy(sdx_taesd* t);
 int sdx_taesd_encode(sdx_taesd* t, const uint8_t* frames, int n, float* latents, void* stream);
 int sdx_taesd_decode(sdx_taesd* t, const float* latents, int n, uint8_t* frames, void* stream);
+/* Per-op device times of the encoder (decoder = 0) or decoder (1) at n live images:
+ * labels[i] (valid until the next call on this thread), flops[i] at n images, ms[i]. */
+int sdx_taesd_profile(sdx_taesd* t, int decoder, int n, int cap, const char** labels, double* flops, float* ms,
+                      int* count);
 int sdx_taesd_param_count(sdx_taesd* t, int* n);
 int sdx_taesd_param(sdx_taesd* t, int i, const char** name, void** ptr, int64_t* shape, int* ndim, int* is_f32);
 /* Measured denoise loop for the bench tables: one CUDA graph of [TAESD encode of

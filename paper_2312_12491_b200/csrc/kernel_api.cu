@@ -290,6 +290,24 @@ int sdx_taesd_decode(sdx_taesd* h, const float* latents, int n, uint8_t* frames,
     });
 }
 
+// Per-op device times of the encoder (decoder = 0) or decoder (1) at n live images.
+int sdx_taesd_profile(sdx_taesd* h, int decoder, int n, int cap, const char** labels, double* flops, float* ms,
+                      int* count) {
+    return kguard([&] {
+        if (!h || n < 1 || n > h->imax) sdx::raise(SDX_INVALID_ARGUMENT, "taesd_profile: 1 <= n <= imax");
+        static thread_local std::vector<std::tuple<std::string, double, float>> res;
+        SDX_CUDA(cudaMemcpy(decoder ? h->dec_cnt : h->enc_cnt, &n, sizeof(int), cudaMemcpyHostToDevice));
+        h->t->profile(decoder != 0, &res);
+        const int k = static_cast<int>(res.size());
+        for (int i = 0; i < k && i < cap; ++i) {
+            labels[i] = std::get<0>(res[static_cast<size_t>(i)]).c_str();
+            flops[i] = std::get<1>(res[static_cast<size_t>(i)]) * n;
+            ms[i] = std::get<2>(res[static_cast<size_t>(i)]);
+        }
+        *count = k;
+    });
+}
+
 int sdx_taesd_param_count(sdx_taesd* h, int* n) {
     return kguard([&] { *n = static_cast<int>(h->t->params().size()); });
 }

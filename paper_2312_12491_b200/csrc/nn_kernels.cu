@@ -630,149 +630,272 @@ __global__ void im2col_kernel(const T* __restrict__ in, long long img_stride, co
     }
 }
 
-// ---- direct 3x3 conv of u8 RGB frames (the TAESD encoder's first layer) -------------
-// One thread = one output pixel x 64 channels on CUDA cores: the 27 inputs (3 rows
-// of 3 pixels x 3 channels, u8 / 255, zero padding) come from a shared row tile,
-// weights [64][K>=27] (column k = tap * 3 + c, as the im2col layout) are staged in smem
-// as fp32 [27][64] and read as broadcast float4s.  Replaces im2col (a 64-column bf16
-// matrix per pixel) + GEMM.
-__global__ void __launch_bounds__(256) conv3x3_rgb8_kernel(const uint8_t* __restrict__ in, long long img_stride,
-                                                           const int* img_src, int H, int W, const bf16* __restrict__ w,
-                                                           int ldw, const float* __restrict__ bias,
-                                                           bf16* __restrict__ out, const int* rows_dev) {
+// ---- warp-level tensor-core helpers (mma.sync m16n8k16, bf16 in, fp32 accumulate) ----------
+// Used by the TAESD head/tail convs, whose 3-channel side is far below a tcgen05 tile
+// (N >= 16 pads 3 to 16+ and the MMA cost is set by the 128-row A operand read).
+__device__ __forceinline__ void mma_bf16_16816(float* d, const uint32_t* a, uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldmatrix_x4(uint32_t* r, const void* smem_row) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_row))));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// ---- 3x3 conv of u8 RGB frames, 3 -> 64 channels (the TAESD encoder's first layer) -------
+// Implicit GEMM on mma.sync.  Persistent blocks (the weights' B fragments are loaded into
+// registers once per block) walk tiles of one image row x 256 pixels; 8 warps x 2
+// fragments of 16 pixels; K = 27 (tap * 3 + channel, as the im2col layout; padded to 32
+// with zero weights), N = 64 (8 n-tiles).  A fragments are gathered in registers straight
+// from a 3-row u8 tile (u8 / 255 -> bf16, zero padding).  The fp32 results (+ bias) are
+// staged as bf16 in shared memory and written with 16-byte coalesced stores: the kernel
+// is bound by its 128 B/pixel output.
+constexpr int kRgbTileW = 256;
+
+__global__ void __launch_bounds__(256, 2) conv3x3_rgb8_kernel(const uint8_t* __restrict__ in, long long img_stride,
+                                                              const int* img_src, int imgs, int H, int W,
+                                                              const bf16* __restrict__ w, int ldw,
+                                                              const float* __restrict__ bias, bf16* __restrict__ out,
+                                                              const int* rows_dev) {
+    constexpr int RS = (kRgbTileW + 2) * 3 + 2;  // row tile stride (bytes)
+    __shared__ uint8_t rowt[3][RS];
+    __shared__ __align__(16) uint8_t ot[kRgbTileW * 128];  // [pixel][8 chunks x 16 B], chunk ^ (pixel & 7)
     pdl_launch();
     pdl_wait();
-    const int n = blockIdx.z, y = blockIdx.y, x0 = blockIdx.x * 256;
-    if (rows_dev && n >= *rows_dev) return;
-    __shared__ __align__(16) float ws[27][64];
-    __shared__ float bs[64];
-    __shared__ uint8_t rowt[3][258 * 3];
-    for (int i = threadIdx.x; i < 27 * 64; i += blockDim.x) {
-        const int k = i / 64, co = i % 64;
-        ws[k][co] = __bfloat162float(w[static_cast<long long>(co) * ldw + k]);
+    const int live = rows_dev ? min(imgs, *rows_dev) : imgs;
+    const int xt = (W + kRgbTileW - 1) / kRgbTileW;
+    const int ntiles = live * H * xt;
+    if (static_cast<int>(blockIdx.x) >= ntiles) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    // B fragments: n-tile j, k-step s -> (k = 16 s + 2 q + {0, 1} (+8), co = 8 j + g)
+    uint32_t bf[8][2][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int k = 16 * s + 2 * q + 8 * h;
+                const bf16* wr = w + static_cast<long long>(8 * j + g) * ldw;
+                const float w0 = k < 27 ? __bfloat162float(wr[k]) : 0.f;
+                const float w1 = k + 1 < 27 ? __bfloat162float(wr[k + 1]) : 0.f;
+                bf[j][s][h] = pack_bf16x2(w0, w1);
+            }
+    float bv[8][2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        bv[j][0] = bias ? bias[8 * j + 2 * q] : 0.f;
+        bv[j][1] = bias ? bias[8 * j + 2 * q + 1] : 0.f;
     }
-    if (threadIdx.x < 64) bs[threadIdx.x] = bias ? bias[threadIdx.x] : 0.f;
-    const uint8_t* base = in + static_cast<long long>(img_src ? img_src[n] : n) * img_stride;
-    for (int i = threadIdx.x; i < 3 * 258 * 3; i += blockDim.x) {
-        const int r = i / (258 * 3), rem = i % (258 * 3);
-        const int xx = x0 - 1 + rem / 3, yy = y - 1 + r;
-        rowt[r][rem] = (yy >= 0 && yy < H && xx >= 0 && xx < W) ? base[(static_cast<long long>(yy) * W + xx) * 3 + rem % 3] : 0;
-    }
-    __syncthreads();
-    const int x = x0 + threadIdx.x;
-    if (x >= W) return;
-    float v[27];
+    // this lane's 8 im2col columns per K-step (k = 16 s + 2 q + {0, 1} + {0, 8}) as offsets
+    // into the flattened row tile (dy * RS + dx * 3 + channel); k >= 27: zero weight
+    int koff[2][4];
 #pragma unroll
-    for (int dy = 0; dy < 3; ++dy)
+    for (int s = 0; s < 2; ++s)
 #pragma unroll
-        for (int dx = 0; dx < 3; ++dx)
+        for (int e = 0; e < 4; ++e) {
+            int k = 16 * s + 2 * q + (e & 1) + 8 * (e >> 1);
+            k = k < 27 ? k : 26;  // any in-tile offset: its weight is zero
+            const int tap = k / 3, ch = k - tap * 3, dy = tap / 3, dx = tap - dy * 3;
+            koff[s][e] = dy * RS + dx * 3 + ch;
+        }
+    const bool vec = (W * 3) % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & 3) == 0 && img_stride % 4 == 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int n = tile / (H * xt), rem = tile - n * H * xt, y = rem / xt, x0 = (rem - y * xt) * kRgbTileW;
+        const uint8_t* base = in + static_cast<long long>(img_src ? img_src[n] : n) * img_stride;
+        {
+            // 3 rows of bytes [(x0 - 1) * 3, (x0 + 257) * 3) with 4-byte loads (rows are W * 3
+            // bytes, a multiple of 4 on the vector path: a word is all in the row or all out)
+            const int b0 = (x0 - 1) * 3;
+            const int w0 = (b0 - 3) / 4;  // floor(b0 / 4) for b0 >= -3
+            const int nw = ((x0 + kRgbTileW + 1) * 3 + 3) / 4 - w0;
+            for (int i = threadIdx.x; i < 3 * nw; i += blockDim.x) {
+                const int r = i / nw, wi = w0 + i % nw, yy = y - 1 + r;
+                const bool rin = yy >= 0 && yy < H;
+                uint32_t v = 0;
+                if (vec) {
+                    if (rin && wi >= 0 && 4 * wi < W * 3)
+                        v = *reinterpret_cast<const uint32_t*>(base + static_cast<long long>(yy) * W * 3 + 4 * wi);
+                } else if (rin) {
+                    for (int e2 = 0; e2 < 4; ++e2) {
+                        const int o = 4 * wi + e2;
+                        if (o >= 0 && o < W * 3) v |= static_cast<uint32_t>(base[static_cast<long long>(yy) * W * 3 + o]) << (8 * e2);
+                    }
+                }
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-                v[(dy * 3 + dx) * 3 + c] = static_cast<float>(rowt[dy][(threadIdx.x + dx) * 3 + c]) * (1.f / 255.f);
-    bf16* op = out + ((static_cast<long long>(n) * H + y) * W + x) * 64;
-#pragma unroll
-    for (int cb = 0; cb < 64; cb += 16) {
-        float acc[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = bs[cb + i];
-#pragma unroll
-        for (int k = 0; k < 27; ++k) {
-#pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-                const float4 wv = *reinterpret_cast<const float4*>(&ws[k][cb + i]);
-                acc[i] = fmaf(v[k], wv.x, acc[i]);
-                acc[i + 1] = fmaf(v[k], wv.y, acc[i + 1]);
-                acc[i + 2] = fmaf(v[k], wv.z, acc[i + 2]);
-                acc[i + 3] = fmaf(v[k], wv.w, acc[i + 3]);
+                for (int e2 = 0; e2 < 4; ++e2) {
+                    const int j = 4 * wi + e2 - b0;
+                    if (j >= 0 && j < (kRgbTileW + 2) * 3) rowt[r][j] = static_cast<uint8_t>(v >> (8 * e2));
+                }
             }
         }
-        store8(op + cb, acc);
-        store8(op + cb + 8, acc + 8);
+        __syncthreads();
+        const uint8_t* rt = &rowt[0][0];
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+            const int p0 = warp * 32 + f * 16;  // first pixel of the fragment (tile column)
+            uint32_t af[2][4];
+#pragma unroll
+            for (int s = 0; s < 2; ++s)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {  // h: pixel p0 + g (+8)
+                    const uint8_t* pp = rt + (p0 + g + 8 * h) * 3;
+                    af[s][h] = pack_bf16x2(pp[koff[s][0]] * (1.f / 255.f), pp[koff[s][1]] * (1.f / 255.f));
+                    af[s][2 + h] = pack_bf16x2(pp[koff[s][2]] * (1.f / 255.f), pp[koff[s][3]] * (1.f / 255.f));
+                }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float d[4] = {bv[j][0], bv[j][1], bv[j][0], bv[j][1]};
+                mma_bf16_16816(d, af[0], bf[j][0][0], bf[j][0][1]);
+                mma_bf16_16816(d, af[1], bf[j][1][0], bf[j][1][1]);
+                // columns 8 j + 2 q, +1 of pixels p0 + g and p0 + g + 8: 4 bytes in chunk j
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int px = p0 + g + 8 * h;
+                    *reinterpret_cast<uint32_t*>(ot + px * 128 + ((j ^ (px & 7)) << 4) + q * 4) =
+                        pack_bf16x2(d[2 * h], d[2 * h + 1]);
+                }
+            }
+        }
+        __syncthreads();
+        bf16* orow = out + (static_cast<long long>(n) * H + y) * W * 64;
+        const int npx = min(kRgbTileW, W - x0);
+        for (int i = threadIdx.x; i < npx * 8; i += blockDim.x) {
+            const int px = i >> 3, ch = i & 7;
+            *reinterpret_cast<uint4*>(orow + static_cast<long long>(x0 + px) * 64 + ch * 8) =
+                *reinterpret_cast<const uint4*>(ot + px * 128 + ((ch ^ (px & 7)) << 4));
+        }
+        // the next tile's row loads overwrite rowt only after this barrier; ot is rewritten
+        // after the next tile's first barrier, once every thread has passed this store loop
     }
 }
 
-// ---- 3x3 conv, 64 -> CO (<= 4) channels, u8 output (TAESD decoder head) ----------------
-// On tensor cores this head pads N to 64 and takes twice a full 64 -> 64 conv (56 vs
-// 31 us per 512^2 image); here it is CUDA-core fp32.  Block = 4 output rows x 128
-// columns; the 6 x 130 x 64 bf16 input tile sits in smem with the 16-byte chunks
-// of each pixel XOR-swizzled by (column % 8), so 32 lanes reading consecutive
-// pixels hit distinct banks; each thread owns 4 pixels (x = p*32 + lane) of its row.
-// Weights as fp32 float4 per (tap, channel) (broadcast reads).  Two blocks per SM
-// overlap one block's tile load with the other's math.
-// fp32 accumulation, then round(255 * clamp(v, 0, 1)) like the GEMM u8 epilogue.
+// ---- 3x3 conv, 64 -> 3 channels, u8 output (TAESD decoder head) --------------------------
+// Implicit GEMM on mma.sync (a tcgen05 tile would pad N = 3 to 64 and cost twice a full
+// 64 -> 64 conv).  Persistent blocks (B fragments of the weights in registers, loaded once)
+// walk tiles of 4 output rows x 128 columns, 8 warps; the 6 x 130 x 64 bf16 input tile
+// sits in smem with the 16-byte chunks of each pixel XOR-swizzled by (column % 8), so the
+// ldmatrix rows (16 consecutive pixels) hit distinct banks.  Each warp owns half a row: 4
+// fragments of 16 pixels accumulated as 4 independent chains of 9 taps x 4 K-steps of
+// m16n8k16 with the 3 (padded to 8) output channels.  fp32 accumulation, then
+// round(255 * clamp(v, 0, 1)) like the GEMM u8 epilogue, staged in smem and written with
+// coalesced 4-byte stores.  Two blocks per SM overlap one block's tile load with the
+// other's math.
 constexpr int kHeadRows = 4;
 constexpr int kHeadTileBytes = (kHeadRows + 2) * 130 * 128;
 
 template <int CO>
-__global__ void __launch_bounds__(32 * kHeadRows) conv3x3_c64_u8_kernel(const bf16* __restrict__ in, int H, int W,
-                                                            const bf16* __restrict__ w, const float* __restrict__ bias,
-                                                            uint8_t* __restrict__ out, const int* img_map,
-                                                            const int* rows_dev) {
+__global__ void __launch_bounds__(64 * kHeadRows, 2) conv3x3_c64_u8_kernel(const bf16* __restrict__ in, int imgs, int H,
+                                                                           int W, const bf16* __restrict__ w,
+                                                                           const float* __restrict__ bias,
+                                                                           uint8_t* __restrict__ out, const int* img_map,
+                                                                           const int* rows_dev) {
     extern __shared__ __align__(16) uint8_t tile[];  // [rows + 2][130][8 chunks x 16 B], swizzled
-    __shared__ __align__(16) float4 ws[9][64];       // (w_o0, w_o1, w_o2, 0) per tap and channel
-    static_assert(CO <= 4, "head conv: <= 4 output channels");
+    __shared__ __align__(16) uint8_t ob[kHeadRows][128 * CO + 4];
+    static_assert(CO <= 8, "head conv: <= 8 output channels");
     pdl_launch();
     pdl_wait();
-    const int n = blockIdx.z;
-    if (rows_dev && n >= *rows_dev) return;
-    const int y0 = blockIdx.y * kHeadRows, x0 = blockIdx.x * 128;
-    for (int i = threadIdx.x; i < 9 * 64; i += blockDim.x) {
-        const int c = i % 64, t = i / 64;
-        float q[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int o = 0; o < CO; ++o) q[o] = __bfloat162float(w[(static_cast<long long>(o) * 9 + t) * 64 + c]);
-        ws[t][c] = make_float4(q[0], q[1], q[2], q[3]);
-    }
-    const bf16* base = in + static_cast<long long>(n) * H * W * 64;
-    for (int i = threadIdx.x; i < (kHeadRows + 2) * 130 * 8; i += blockDim.x) {
-        const int k = i & 7, col = (i >> 3) % 130, r = i / (130 * 8);
-        const int yy = y0 - 1 + r, xx = x0 - 1 + col;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (yy >= 0 && yy < H && xx >= 0 && xx < W) v = *reinterpret_cast<const uint4*>(base + (static_cast<long long>(yy) * W + xx) * 64 + k * 8);
-        *reinterpret_cast<uint4*>(tile + ((r * 130 + col) * 8 + (k ^ (col & 7))) * 16) = v;
-    }
-    __syncthreads();
-    const int ty = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    float acc[4][CO];
+    const int live = rows_dev ? min(imgs, *rows_dev) : imgs;
+    const int xt = (W + 127) / 128, yt = (H + kHeadRows - 1) / kHeadRows;
+    const int ntiles = live * yt * xt;
+    if (static_cast<int>(blockIdx.x) >= ntiles) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, q = lane & 3;
+    // B fragments: tap t, K-step s (channels 16 s ..), h: k = 16 s + 2 q + 8 h + {0, 1}, co = g
+    uint32_t bf[9][4][2];
 #pragma unroll
-    for (int p = 0; p < 4; ++p)
+    for (int t = 0; t < 9; ++t)
 #pragma unroll
-        for (int o = 0; o < CO; ++o) acc[p][o] = bias ? bias[o] : 0.f;
-#pragma unroll 1
-    for (int t = 0; t < 9; ++t) {
-        const int dy = t / 3, dx = t % 3;
-#pragma unroll 2
-        for (int k = 0; k < 8; ++k) {
-            float wv[8][4];
+        for (int s = 0; s < 4; ++s)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float4 q = ws[t][k * 8 + j];
-                wv[j][0] = q.x;
-                wv[j][1] = q.y;
-                wv[j][2] = q.z;
-                wv[j][3] = q.w;
+            for (int h = 0; h < 2; ++h) {
+                const int ci = 16 * s + 2 * q + 8 * h;
+                const bf16* wr = w + (static_cast<long long>(g) * 9 + t) * 64 + ci;
+                bf[t][s][h] = g < CO ? pack_bf16x2(__bfloat162float(wr[0]), __bfloat162float(wr[1])) : 0u;
             }
+    const float bias0 = (bias && 2 * q < CO) ? bias[2 * q] : 0.f;
+    const float bias1 = (bias && 2 * q + 1 < CO) ? bias[2 * q + 1] : 0.f;
+    const int ty = warp >> 1, half = warp & 1;
+    // ldmatrix.x4 row address of this lane: fragment row (lane & 15), chunk half (lane >> 4)
+    const int lrow = lane & 15, lchunk = lane >> 4;
+    for (int tl = blockIdx.x; tl < ntiles; tl += gridDim.x) {
+        const int n = tl / (yt * xt), rem = tl - n * yt * xt, by = rem / xt;
+        const int y0 = by * kHeadRows, x0 = (rem - by * xt) * 128;
+        const bf16* base = in + static_cast<long long>(n) * H * W * 64;
+        // the whole tile in flight at once: 16-byte cp.async (zero-filled outside the image)
+        for (int i = threadIdx.x; i < (kHeadRows + 2) * 130 * 8; i += blockDim.x) {
+            const int k = i & 7, col = (i >> 3) % 130, r = i / (130 * 8);
+            const int yy = y0 - 1 + r, xx = x0 - 1 + col;
+            const bool inb = yy >= 0 && yy < H && xx >= 0 && xx < W;
+            const bf16* src = inb ? base + (static_cast<long long>(yy) * W + xx) * 64 + k * 8 : base;
+            const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(tile + ((r * 130 + col) * 8 + (k ^ (col & 7))) * 16));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(inb ? 16 : 0) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        // the warp's 4 fragments (16 columns each) accumulate independently: 4 MMA chains in
+        // flight per warp instead of one dependent chain of 36
+        float d[4][4];
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
-                const int col = p * 32 + lane + dx;
-                float v[8];
-                unpack8(*reinterpret_cast<const uint4*>(tile + (((ty + dy) * 130 + col) * 8 + (k ^ (col & 7))) * 16), v);
+        for (int f = 0; f < 4; ++f) {
+            d[f][0] = bias0;
+            d[f][1] = bias1;
+            d[f][2] = bias0;
+            d[f][3] = bias1;
+        }
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
+        for (int t = 0; t < 9; ++t) {
+            const int dy = t / 3, dx = t - dy * 3;
 #pragma unroll
-                    for (int o = 0; o < CO; ++o) acc[p][o] = fmaf(v[j], wv[j][o], acc[p][o]);
+            for (int s = 0; s < 4; ++s) {
+#pragma unroll
+                for (int f = 0; f < 4; ++f) {
+                    const int col = half * 64 + f * 16 + lrow + dx;
+                    uint32_t af[4];
+                    // matrices: (rows 0-7, k 0-7), (rows 8-15, k 0-7), (rows 0-7, k 8-15), (rows 8-15, k 8-15)
+                    ldmatrix_x4(af, tile + ((ty + dy) * 130 + col) * 128 + (((2 * s + lchunk) ^ (col & 7)) << 4));
+                    mma_bf16_16816(d[f], af, bf[t][s][0], bf[t][s][1]);
+                }
             }
         }
-    }
-    const int y = y0 + ty;
-    if (y >= H) return;
-    uint8_t* ob = out + (static_cast<long long>(img_map ? img_map[n] : n) * H + y) * W * CO;
 #pragma unroll
-    for (int p = 0; p < 4; ++p) {
-        const int x = x0 + p * 32 + lane;
-        if (x >= W) continue;
+        for (int f = 0; f < 4; ++f) {
+            const int c0 = half * 64 + f * 16;
+            // d[f]: (pixel c0 + g, channels 2q, 2q+1), (pixel c0 + g + 8, same)
 #pragma unroll
-        for (int o = 0; o < CO; ++o)
-            ob[static_cast<long long>(x) * CO + o] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(acc[p][o], 0.f), 1.f) * 255.f));
+            for (int h = 0; h < 2; ++h) {
+                const int px = c0 + g + 8 * h;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int o = 2 * q + e;
+                    if (o < CO)
+                        ob[ty][px * CO + o] = static_cast<uint8_t>(__float2int_rn(fminf(fmaxf(d[f][2 * h + e], 0.f), 1.f) * 255.f));
+                }
+            }
+        }
+        __syncthreads();  // tile consumed, ob complete
+        // coalesced write-out: each row of the block is 128 * CO contiguous bytes
+        const int nx = min(128, W - x0);
+        for (int r = 0; r < kHeadRows; ++r) {
+            const int y = y0 + r;
+            if (y >= H) break;
+            uint8_t* orow = out + ((static_cast<long long>(img_map ? img_map[n] : n) * H + y) * W + x0) * CO;
+            if (nx == 128 && (128 * CO) % 4 == 0 && (reinterpret_cast<uintptr_t>(orow) & 3) == 0) {
+                for (int i = threadIdx.x; i < 32 * CO; i += blockDim.x)
+                    reinterpret_cast<uint32_t*>(orow)[i] = *reinterpret_cast<const uint32_t*>(&ob[r][4 * i]);
+            } else {
+                for (int i = threadIdx.x; i < nx * CO; i += blockDim.x) orow[i] = ob[r][i];
+            }
+        }
+        __syncthreads();  // ob read before the next tile's fragments overwrite it
     }
 }
 
@@ -1015,16 +1138,20 @@ void run_im2col3x3_u8(const uint8_t* in, long long img_stride, const int* img_sr
 void run_conv3x3_rgb8(const uint8_t* in, long long img_stride, const int* img_src, int imgs, int H, int W,
                       const bf16* w, int ldw, const float* bias, bf16* out, const int* rows_dev, cudaStream_t st) {
     if (ldw < 27) raise(SDX_INVALID_ARGUMENT, "conv3x3_rgb8: weight row shorter than 27");
-    launch_pdl(conv3x3_rgb8_kernel, dim3((W + 255) / 256, H, imgs), dim3(256), 0, st, in, img_stride, img_src, H, W, w,
-               ldw, bias, out, rows_dev);
+    const long long tiles = static_cast<long long>(imgs) * H * ((W + kRgbTileW - 1) / kRgbTileW);
+    const int grid = static_cast<int>(std::min<long long>(tiles, 2LL * kSmCount));
+    launch_pdl(conv3x3_rgb8_kernel, dim3(grid), dim3(256), 0, st, in, img_stride, img_src, imgs, H, W, w, ldw, bias,
+               out, rows_dev);
 }
 
 void run_conv3x3_c64_u8(const bf16* in, int imgs, int H, int W, const bf16* w, int Cout, const float* bias,
                         uint8_t* out, const int* img_map, const int* rows_dev, cudaStream_t st) {
     if (Cout != 3) raise(SDX_INVALID_ARGUMENT, "conv3x3_c64_u8: 3 output channels");
     ensure_kernel_attrs(conv3x3_c64_u8_kernel<3>, kHeadTileBytes);
-    launch_pdl(conv3x3_c64_u8_kernel<3>, dim3((W + 127) / 128, (H + kHeadRows - 1) / kHeadRows, imgs), dim3(32 * kHeadRows),
-               static_cast<size_t>(kHeadTileBytes), st, in, H, W, w, bias, out, img_map, rows_dev);
+    const long long tiles = static_cast<long long>(imgs) * ((H + kHeadRows - 1) / kHeadRows) * ((W + 127) / 128);
+    const int grid = static_cast<int>(std::min<long long>(tiles, 2LL * kSmCount));
+    launch_pdl(conv3x3_c64_u8_kernel<3>, dim3(grid), dim3(64 * kHeadRows), static_cast<size_t>(kHeadTileBytes), st, in,
+               imgs, H, W, w, bias, out, img_map, rows_dev);
 }
 
 void run_timestep_embedding(const int* taus, int n, int dim, bf16* out, cudaStream_t st) {

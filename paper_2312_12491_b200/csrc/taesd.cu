@@ -45,8 +45,12 @@ void TAESD::conv(std::vector<Op>& ops, double& flops, const bf16* x, int H, int 
     e.rows_per_unit = static_cast<long long>(Ho) * Ho;
     bf16* w = wbf(nm + ".w", {kC, 3, 3, kC}, std::sqrt(2.f / (9.f * kC)));
     GemmPlan p = plan_conv3x3(x, imax_, H, H, kC, w, kC, stride, e);
-    ops.push_back(Op{"conv3x3", [p](cudaStream_t s) { run_gemm(p, s); }});
-    flops += 2.0 * Ho * Ho * kC * 9.0 * kC;
+    const double f = 2.0 * Ho * Ho * kC * 9.0 * kC;
+    ops.push_back(Op{"conv3x3", [p](cudaStream_t s) { run_gemm(p, s); },
+                     "conv3x3 " + std::to_string(Ho) + "^2 s" + std::to_string(stride) + " bn=" + std::to_string(p.bn) +
+                         (p.amode == kAHalo ? " halo" : ""),
+                     f});
+    flops += f;
 }
 
 int TAESD::block(std::vector<Op>& ops, double& flops, int r, int in, const std::string& nm, const int* count) {
@@ -87,7 +91,7 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             bf16* o = buf(0, 0);
             enc_.push_back(Op{"conv_in", [=](cudaStream_t s) {
                                   run_conv3x3_rgb8(fr, fs, src, im, 512, 512, w, 64, b, o, cnt, s);
-                              }});
+                              }, "conv_in 512^2 rgb8", 2.0 * 512 * 512 * kC * 27});
             enc_flops_ += 2.0 * 512 * 512 * kC * 27;
         }
         int cur = block(enc_, enc_flops_, 0, 0, "enc.b0", cnt);
@@ -108,7 +112,8 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             e.rows_per_unit = 64 * 64;
             bf16* w = wbf("enc.conv_out.w", {4, 3, 3, kC}, std::sqrt(1.f / (9.f * kC)));
             GemmPlan p = plan_conv3x3(buf(3, cur), imax_, 64, 64, kC, w, 4, 1, e);
-            enc_.push_back(Op{"conv_out", [p](cudaStream_t s) { run_gemm(p, s); }});
+            enc_.push_back(Op{"conv_out", [p](cudaStream_t s) { run_gemm(p, s); }, "conv_out 64^2 64->4",
+                              2.0 * 64 * 64 * 4 * 9.0 * kC});
             enc_flops_ += 2.0 * 64 * 64 * 4 * 9.0 * kC;
         }
     }
@@ -123,7 +128,7 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             bf16* a0 = a0_;
             dec_.push_back(Op{"im2col", [=](cudaStream_t s) {
                                   run_im2col3x3_f32_gather(li, 64 * 64 * 4, src, im, 64, 64, 4, 64, 1, a0, cnt, s);
-                              }});
+                              }, "im2col 64^2", 0.0});
         }
         {
             GemmEpilogue e;
@@ -134,7 +139,8 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             e.rows_per_unit = 64 * 64;
             bf16* w = wbf("dec.conv_in.w", {kC, 64}, std::sqrt(2.f / 36.f));
             GemmPlan p = plan_gemm(a0_, 64, w, 64, imax_ * 64 * 64, kC, 64, e);
-            dec_.push_back(Op{"conv_in", [p](cudaStream_t s) { run_gemm(p, s); }});
+            dec_.push_back(Op{"conv_in", [p](cudaStream_t s) { run_gemm(p, s); }, "conv_in 64^2 4->64",
+                              2.0 * 64 * 64 * kC * 36});
             dec_flops_ += 2.0 * 64 * 64 * kC * 36;
         }
         int cur = 0;
@@ -145,7 +151,8 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             bf16* up = buf(r, 2);
             const int Hs = kRes[r + 1];
             const int im = imax_;
-            dec_.push_back(Op{"upsample", [=](cudaStream_t s) { run_upsample2x(src, im, Hs, Hs, kC, up, cnt, s); }});
+            dec_.push_back(Op{"upsample", [=](cudaStream_t s) { run_upsample2x(src, im, Hs, Hs, kC, up, cnt, s); },
+                              "upsample " + std::to_string(Hs) + "^2->" + std::to_string(2 * Hs) + "^2", 0.0});
             conv(dec_, dec_flops_, up, kRes[r], 1, "dec.up" + std::to_string(r), false, kActNone, nullptr, buf(r, 0), cnt);
             cur = 0;
             const int nblocks = r == 0 ? 1 : 3;
@@ -160,7 +167,8 @@ TAESD::TAESD(int imax, uint64_t seed, const TaesdIO& io, cudaStream_t st) : imax
             uint8_t* fo = io.frames_out;
             const int* map = io.dec_dst;
             const int im = imax_;
-            dec_.push_back(Op{"conv_out", [=](cudaStream_t s) { run_conv3x3_c64_u8(x, im, 512, 512, w, 3, b, fo, map, cnt, s); }});
+            dec_.push_back(Op{"conv_out", [=](cudaStream_t s) { run_conv3x3_c64_u8(x, im, 512, 512, w, 3, b, fo, map, cnt, s); },
+                              "conv_out 512^2 64->3 u8", 2.0 * 512 * 512 * 3 * 9.0 * kC});
             dec_flops_ += 2.0 * 512 * 512 * 3 * 9.0 * kC;
         }
     }
@@ -180,6 +188,40 @@ void TAESD::encode(cudaStream_t st) {
 
 void TAESD::decode(cudaStream_t st) {
     for (auto& op : dec_) op.fn(st);
+}
+
+void TAESD::profile(bool decoder, std::vector<std::tuple<std::string, double, float>>* out) {
+    constexpr int kReps = 10;
+    std::vector<Op>& ops = decoder ? dec_ : enc_;
+    cudaStream_t cs;
+    SDX_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaEvent_t e0, e1;
+    SDX_CUDA(cudaEventCreate(&e0));
+    SDX_CUDA(cudaEventCreate(&e1));
+    for (auto& op : ops) op.fn(cs);
+    SDX_CUDA(cudaStreamSynchronize(cs));
+    out->clear();
+    for (auto& op : ops) {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        SDX_CUDA(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+        for (int r = 0; r < kReps; ++r) op.fn(cs);
+        SDX_CUDA(cudaStreamEndCapture(cs, &graph));
+        SDX_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+        SDX_CUDA(cudaGraphLaunch(exec, cs));
+        SDX_CUDA(cudaEventRecord(e0, cs));
+        SDX_CUDA(cudaGraphLaunch(exec, cs));
+        SDX_CUDA(cudaEventRecord(e1, cs));
+        SDX_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        SDX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        out->emplace_back(op.label, op.flops, ms / kReps);
+        cudaGraphExecDestroy(exec);
+        cudaGraphDestroy(graph);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(cs);
 }
 
 }  // namespace sdx

@@ -19,6 +19,7 @@
 
 #include <functional>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "gemm_sm100.cuh"
@@ -59,11 +60,17 @@ class TAESD {
     double dec_flops_per_image() const { return dec_flops_; }
     int launches_per_encode() const { return static_cast<int>(enc_.size()); }
     int launches_per_decode() const { return static_cast<int>(dec_.size()); }
+    // Per-op device times of the encoder (decoder=false) or decoder at the live image
+    // count already set on the device: each op alone, 10 back-to-back repetitions in one
+    // CUDA graph (as UNet::forward_profiled).  out: (label, flops per image, ms).
+    void profile(bool decoder, std::vector<std::tuple<std::string, double, float>>* out);
 
   private:
     struct Op {
         std::string kind;
         std::function<void(cudaStream_t)> fn;
+        std::string label;  // kind + resolution (per-op profile)
+        double flops = 0;   // per image
     };
     bf16* wbf(const std::string& name, std::vector<long long> shape, float std);
     float* wf32(const std::string& name, std::vector<long long> shape, float std);

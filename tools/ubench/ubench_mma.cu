@@ -104,6 +104,8 @@ void run(long long* d, const char* name) {
 int main() {
     long long* d;
     cudaMalloc(&d, 296 * sizeof(long long));
+    run<1, 0, 16>(d, "SS warp+elect");
+    run<1, 0, 32>(d, "SS warp+elect");
     run<0, 0, 64>(d, "SS lane0-divergent");
     run<1, 0, 64>(d, "SS warp+elect");
     run<0, 0, 128>(d, "SS lane0-divergent");
