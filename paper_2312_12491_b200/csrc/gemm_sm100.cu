@@ -37,8 +37,7 @@ struct GemmArgs {
     int splits;   // split-K factor (> 1: raw fp32 partials to ws, epilogue in splitk_reduce)
     float* ws;    // [splits][M][N]
     unsigned long long* dbg;  // optional per-CTA phase timestamps [grid][16] (kernel benchmarks)
-    int xmode;                // experiments only: 1 = no MMAs issued, 2 = no TMA loads, 3 = conv boxes moved in bounds (probes)
-    int whint;                // B (weights) loaded with an L2 evict_first policy
+    int xmode;                // experiments only: 1 = no MMAs issued, 2 = no TMA loads (pipeline probes)
     int wpre;                 // first B slices issued before the PDL wait
     GemmEpilogue epi;
 };
@@ -64,7 +63,7 @@ __device__ __forceinline__ void wait_bounded(uint64_t* bar, uint32_t phase) {
     // mbarrier wait with a watchdog: a protocol bug traps instead of hanging the GPU
     const uint32_t a = smem_u32(bar);
     uint32_t done = 0;
-    long long t0 = clock64();
+    long long t0 = 0;  // read only once the first try fails (off the common path)
     while (true) {
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
@@ -74,7 +73,9 @@ __device__ __forceinline__ void wait_bounded(uint64_t* bar, uint32_t phase) {
             : "r"(a), "r"(phase)
             : "memory");
         if (done) return;
-        if (clock64() - t0 > (1LL << 33)) {
+        if (t0 == 0) {
+            t0 = clock64();
+        } else if (clock64() - t0 > (1LL << 33)) {
             printf("sdx gemm: mbarrier watchdog fired (block %d,%d thread %d)\n", blockIdx.x, blockIdx.y,
                    threadIdx.x);
             asm volatile("trap;");
@@ -234,12 +235,9 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                 const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
                 const int n0 = (t % n_tiles) * BN;
                 npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
-                const uint64_t wpol = l2_policy_evict_first();
                 for (int i = 0; i < npre; ++i) {
-                    const int kb = kb0 + i;
                     mbar_expect_tx_only(&full[i], B_BYTES);
-                    if (g.whint) tma_load_2d_hint(sB + i * B_BYTES, &tb, &full[i], kb * BK, n0, wpol);
-                    else tma_load_2d(sB + i * B_BYTES, &tb, &full[i], kb * BK, n0);
+                    tma_load_2d(sB + i * B_BYTES, &tb, &full[i], (kb0 + i) * BK, n0);
                 }
             }
         }
@@ -307,9 +305,12 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
         __syncwarp();
     } else if (warp == 0) {
         if (lane == 0) {
+            // Lean issue loop (this single thread paces the TMA stream; its per-slice issue
+            // latency bounded the convs): stage ring position and conv tap / channel-block
+            // coordinates advance incrementally, no divisions per K slice.
             const int cblocks = AMODE == kAConv ? g.Cin / BK : 1;
-            const uint64_t wpol = l2_policy_evict_first();
-            uint32_t it = 0;
+            int s = 0;
+            uint32_t ph = 0, it = 0;
             if (npre > 0 && ustart >= total) {
                 // the live row count dropped this CTA's first unit: drain the prefetched B
                 for (int i = 0; i < npre; ++i) mbar_arrive(&full[i]);
@@ -320,70 +321,55 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                 const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
                 const int m0 = (t / n_tiles) * MU + static_cast<int>(rank) * BM;
                 const int n0 = (t % n_tiles) * BN + static_cast<int>(rank) * BNL;
-                int cn0 = 0, cy0 = 0, cx0 = 0;
+                int cn0 = 0, ax = 0, ay = 0, cb = 0, dx = 0;
                 if (AMODE == kAConv) {
                     const int hw = g.Ho * g.Wo;
                     cn0 = m0 / hw;
                     const int rem = m0 - cn0 * hw;
-                    cy0 = rem / g.Wo;
-                    cx0 = rem - cy0 * g.Wo;
+                    const int cy0 = rem / g.Wo, cx0 = rem - cy0 * g.Wo;
+                    const int tap = kb0 / cblocks, dy = tap / 3;
+                    cb = kb0 - tap * cblocks;
+                    dx = tap - dy * 3;
+                    ax = cx0 * g.stride + dx - 1;  // box origin of the current tap
+                    ay = cy0 * g.stride + dy - 1;
                 }
+                const int k1b = AMODE == kAConcat ? g.K1 / BK : 0;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
                     wait_bounded(&empty[s], ph ^ 1);
                     uint8_t* dA = sA + s * A_BYTES;
-                    int ac0, ac1, ac2 = 0, ac3 = 0;  // A box coordinates
-                    const CUtensorMap* amap = &ta;
-                    if (AMODE == kAMatrix) {
-                        ac0 = kb * BK;
-                        ac1 = m0;
-                    } else if (AMODE == kAConcat) {
-                        const int k1b = g.K1 / BK;
-                        if (kb < k1b) {
-                            ac0 = kb * BK;
-                        } else {
-                            ac0 = (kb - k1b) * BK;
-                            amap = &ta2;
-                        }
-                        ac1 = m0;
-                    } else {
-                        const int tap = kb / cblocks;
-                        const int cb = kb - tap * cblocks;
-                        const int dy = tap / 3, dx = tap - dy * 3;
-                        ac0 = cb * BK;
-                        ac1 = cx0 * g.stride + dx - 1;
-                        ac2 = cy0 * g.stride + dy - 1;
-                        ac3 = cn0;
-                        if (g.xmode == 3) {  // probe: the same boxes moved in bounds (wrong results)
-                            ac1 = ac1 < 0 ? 0 : ac1;
-                            ac1 = ac1 + g.Wt * g.stride > g.Wo * g.stride ? g.Wo * g.stride - g.Wt * g.stride : ac1;
-                            ac2 = ac2 < 0 ? 0 : ac2;
-                            ac2 = ac2 + g.Ht * g.stride > g.Ho * g.stride ? g.Ho * g.stride - g.Ht * g.stride : ac2;
-                        }
-                    }
                     if (g.xmode == 2) {  // probe: skip the loads
                         if (rank == 0) mbar_arrive(&full[s]);
-                        continue;
-                    }
-                    if constexpr (PAIR) {
-                        // both CTAs' loads complete on the leader's full barrier
-                        const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
-                        if (rank == 0) mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
-                        if (AMODE == kAConv) tma_load_4d_pair(dA, amap, fb, ac0, ac1, ac2, ac3);
-                        else tma_load_2d_pair(dA, amap, fb, ac0, ac1);
-                        if (g.whint) tma_load_2d_pair_hint(sB + s * B_BYTES, &tb, fb, kb * BK, n0, wpol);
-                        else tma_load_2d_pair(sB + s * B_BYTES, &tb, fb, kb * BK, n0);
-                    } else if (static_cast<int>(it) < npre) {  // B already in flight (prefetched)
-                        mbar_expect_tx(&full[s], A_BYTES);
-                        if (AMODE == kAConv) tma_load_4d(dA, amap, &full[s], ac0, ac1, ac2, ac3);
-                        else tma_load_2d(dA, amap, &full[s], ac0, ac1);
                     } else {
-                        mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-                        if (AMODE == kAConv) tma_load_4d(dA, amap, &full[s], ac0, ac1, ac2, ac3);
-                        else tma_load_2d(dA, amap, &full[s], ac0, ac1);
-                        if (g.whint) tma_load_2d_hint(sB + s * B_BYTES, &tb, &full[s], kb * BK, n0, wpol);
-                        else tma_load_2d(sB + s * B_BYTES, &tb, &full[s], kb * BK, n0);
+                        const CUtensorMap* amap = (AMODE == kAConcat && kb >= k1b) ? &ta2 : &ta;
+                        const int ac0 = AMODE == kAConv ? cb * BK : (AMODE == kAConcat && kb >= k1b ? kb - k1b : kb) * BK;
+                        if constexpr (PAIR) {
+                            // both CTAs' loads complete on the leader's full barrier
+                            const uint32_t fb = mapa_shared(smem_u32(&full[s]), 0);
+                            if (rank == 0) mbar_expect_tx(&full[s], 2 * (A_BYTES + B_BYTES));
+                            if (AMODE == kAConv) tma_load_4d_pair(dA, amap, fb, ac0, ax, ay, cn0);
+                            else tma_load_2d_pair(dA, amap, fb, ac0, m0);
+                            tma_load_2d_pair(sB + s * B_BYTES, &tb, fb, kb * BK, n0);
+                        } else {
+                            const bool bpre = static_cast<int>(it) < npre;  // B already in flight (prefetched)
+                            mbar_expect_tx(&full[s], bpre ? A_BYTES : A_BYTES + B_BYTES);
+                            if (AMODE == kAConv) tma_load_4d(dA, amap, &full[s], ac0, ax, ay, cn0);
+                            else tma_load_2d(dA, amap, &full[s], ac0, m0);
+                            if (!bpre) tma_load_2d(sB + s * B_BYTES, &tb, &full[s], kb * BK, n0);
+                        }
+                    }
+                    if (AMODE == kAConv && ++cb == cblocks) {  // next tap
+                        cb = 0;
+                        if (++dx == 3) {
+                            dx = 0;
+                            ax -= 2;
+                            ay += 1;
+                        } else {
+                            ax += 1;
+                        }
+                    }
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
                     }
                 }
             }
@@ -391,7 +377,8 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
     } else if (warp == 1) {
         if (rank == 0) {  // converged warp, elected-lane issue; CTA pair: only the leader issues
             constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN);
-            uint32_t it = 0, lt = 0;
+            uint32_t it = 0, lt = 0, ph = 0;
+            int s = 0;  // stage ring position (advanced incrementally, as the producer's)
             for (int u = ustart; u < total; u += ustep, ++lt) {
                 const int sp = u % splits;
                 const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
@@ -400,8 +387,6 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                 tc_fence_after();
                 const uint32_t dtm = tmem + acc * BN;
                 for (int kb = kb0; kb < kb1; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
                     wait_bounded(&full[s], ph);
                     if (dbg && it == 0 && lane == 0) dbg[2] = gtimer();
                     tc_fence_after();
@@ -414,6 +399,10 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                     }
                     if (PAIR) umma_commit_pair_el(&empty[s], 3);
                     else umma_commit_el(&empty[s]);
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
                 }
                 if (PAIR) umma_commit_pair_el(&tfull[acc], 3);
                 else umma_commit_el(&tfull[acc]);
@@ -1119,12 +1108,6 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
     g.ws = p.ws;
     g.dbg = g_dbg;
     g.xmode = g_xmode;
-    // SDX_WHINT=1: weights with an L2 evict_first hint (measured: +0.5% at 4 rows, -0.9% at 8)
-    static const int whint = [] {
-        const char* v = std::getenv("SDX_WHINT");
-        return v && v[0] == '1' ? 1 : 0;
-    }();
-    g.whint = whint;
     // SDX_WPREFETCH=0: no weight loads before the PDL wait
     static const int wpre = [] {
         const char* v = std::getenv("SDX_WPREFETCH");

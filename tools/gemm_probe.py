@@ -16,15 +16,14 @@ L.sdx_kernel_gemm_probe.argtypes = [C.c_int]
 
 def probe(label, make, flops):
     res = []
-    for mode in (0, 1, 2) + ((3,) if label.startswith("conv") else ()):
+    for mode in (0, 1, 2):
         L.sdx_kernel_gemm_probe(mode)
         h = vp()
         assert make(C.byref(h)) == 0, L.sdx_kernel_last_error()
         res.append(time_plan(h))
         L.sdx_kernel_plan_destroy(h)
     L.sdx_kernel_gemm_probe(0)
-    print(f"{label:48s} full {res[0]:7.1f} us ({flops / res[0] / 1e6:6.1f} TF/s) | tma-only {res[1]:7.1f} | mma-only {res[2]:7.1f}"
-          + (f" | in-bounds boxes {res[3]:7.1f}" if len(res) > 3 else ""),
+    print(f"{label:48s} full {res[0]:7.1f} us ({flops / res[0] / 1e6:6.1f} TF/s) | tma-only {res[1]:7.1f} | mma-only {res[2]:7.1f}",
           flush=True)
 
 
