@@ -155,7 +155,14 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
         shortcut = s;
         // The shortcut depends only on the block input: run it on the side stream from the
         // start of the block (graph branch), concurrent with GN1 -> conv1 -> GN2, and join
-        // before conv2, which adds it as the residual.
+        // before conv2, which adds it as the residual.  SDX_FORK=0: inline on the main
+        // stream (one programmatic-launch chain, no cross-stream edges).
+        static const bool fork_on = [] {
+            const char* v = std::getenv("SDX_FORK");
+            return !(v && v[0] == '0');
+        }();
+        if (!fork_on) goto conv2;
+        {
         Op sc = ops_.back();
         ops_.pop_back();
         cudaEvent_t ea, eb;
@@ -174,7 +181,9 @@ bf16* UNet::resblock(const bf16* x, int Cx, const bf16* skip, int Cs, int Cout, 
         sc.join = [=](cudaStream_t st) { SDX_CUDA(cudaStreamWaitEvent(st, eb, 0)); };
         ops_.insert(ops_.begin() + static_cast<long>(fork_at), sc);
         ops_.push_back(Op{"join", [=](cudaStream_t st) { SDX_CUDA(cudaStreamWaitEvent(st, eb, 0)); }, "join", 0.0, nullptr});
+        }
     }
+conv2:
     bf16* out = act(M * Cout);
     {
         bf16* w = wbf(nm + ".conv2.w", {Cout, 3, 3, Cout}, 1.f / std::sqrt(9.f * Cout));

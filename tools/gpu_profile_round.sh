@@ -11,5 +11,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 python tools/ncu_traffic.py gpurun_out/unet_traffic_r8.csv gpurun_out/unet_traffic_r8.json "UNet forward, 8 rows (cfg4 denoiser launch)" 8 > gpurun_out/unet_traffic_r8.txt
 NCU="ncu --set full $M --import-source on"
 timeout 600 $NCU -k regex:gemm_tc -s 12 -c 1 --profile-from-start off -o gpurun_out/ncu_full_gemm python tools/prof_unet.py 4 2 > gpurun_out/ncu_full_gemm.log 2>&1
-timeout 600 $NCU -k regex:attn_kernel -s 0 -c 1 --profile-from-start off -o gpurun_out/ncu_full_attn python tools/prof_unet.py 4 2 > gpurun_out/ncu_full_attn.log 2>&1
+timeout 600 $NCU -k regex:attn -s 0 -c 1 --profile-from-start off -o gpurun_out/ncu_full_attn python tools/prof_unet.py 4 2 > gpurun_out/ncu_full_attn.log 2>&1
 ls -la gpurun_out
