@@ -306,7 +306,9 @@ __device__ __forceinline__ float ld_dsmem_f32(const float* local, uint32_t rank)
     uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(local)), r;
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
     float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(r) : "memory");
+    // not volatile: independent remote loads may be issued back to back (ordering against
+    // the partials' producers comes from the cluster barrier before the first call)
+    asm("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(r));
     return v;
 }
 
@@ -428,10 +430,20 @@ __global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
     if (threadIdx.x < p.groups) {
         const int g = threadIdx.x;
+        // all ranks' partials requested at once (independent DSMEM loads, <= 16 ranks), then
+        // added in rank order: one remote round trip instead of one per rank
+        float pa[16], pb[16];
+        const uint32_t nr = gridDim.x;  // grid.x == cluster size
+#pragma unroll
+        for (uint32_t r = 0; r < 16; ++r) {
+            pa[r] = r < nr ? ld_dsmem_f32(&gpart[2 * g], r) : 0.f;
+            pb[r] = r < nr ? ld_dsmem_f32(&gpart[2 * g + 1], r) : 0.f;
+        }
         double a = 0.0, b = 0.0;
-        for (uint32_t r = 0; r < gridDim.x; ++r) {  // grid.x == cluster size
-            a += static_cast<double>(ld_dsmem_f32(&gpart[2 * g], r));
-            b += static_cast<double>(ld_dsmem_f32(&gpart[2 * g + 1], r));
+#pragma unroll
+        for (uint32_t r = 0; r < 16; ++r) {
+            a += static_cast<double>(pa[r]);
+            b += static_cast<double>(pb[r]);
         }
         const double n = static_cast<double>(cg) * p.HW;
         const double m = a / n;
