@@ -37,7 +37,7 @@ struct GemmArgs {
     int splits;   // split-K factor (> 1: raw fp32 partials to ws, epilogue in splitk_reduce)
     float* ws;    // [splits][M][N]
     unsigned long long* dbg;  // optional per-CTA phase timestamps [grid][16] (kernel benchmarks)
-    int xmode;                // experiments only: 1 = no MMAs issued, 2 = no TMA loads (pipeline probes)
+    int xmode;                // experiments only: 1 = no MMAs issued, 2 = no TMA loads, 4 = no epilogue (probes)
     int wpre;                 // first B slices issued before the PDL wait
     GemmEpilogue epi;
 };
@@ -481,6 +481,15 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
             wait_bounded(&tfull[acc], (lt >> 1) & 1);
             if (dbg && lt == 0 && warp == 2 && lane == 0) dbg[4] = gtimer();
             tc_fence_after();
+            if (g.xmode == 4) {  // probe: no epilogue work (results wrong)
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR) mbar_arrive_cluster(mapa_shared(smem_u32(&tempty[acc]), 0));
+                    else mbar_arrive(&tempty[acc]);
+                }
+                continue;
+            }
             float rs_sum = 0.f, rs_sq = 0.f;  // row statistics of this tile's stored values
             const uint32_t tbase = tmem + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1

@@ -113,7 +113,7 @@ void set_gemm_tiling_override(int bn, int splits, int pair = 0);
 // stamps per CTA (entry, setup done, first stage landed, first tile committed,
 // epilogue start / end, exit); null disables.  Kernel benchmarks only.
 void set_gemm_debug_buffer(unsigned long long* dbg);
-// Pipeline probes (results wrong): 1 = TMA only (no MMAs), 2 = MMA only (no loads).
+// Pipeline probes (results wrong): 1 = TMA only (no MMAs), 2 = MMA only (no loads), 4 = no epilogue work.
 void set_gemm_probe_mode(int mode);
 // Modelled cost (SM clocks) of one tiling; see choose_tiling in gemm_sm100.cu.
 double gemm_cost(long long M, int N, int K, int bn, int splits, int out_bytes, bool residual, bool pair);

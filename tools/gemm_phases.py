@@ -66,6 +66,10 @@ def conv(imgs, H, cin, cout, stride=1):
                                              out.data_ptr(), 0, 0, 0, hp))
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "taesd":
+    conv(8, 512, 64, 64)
+    conv(1, 512, 64, 64)
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "small":
     # the UNet's small-K linears at 4 rows
     gemm(16384, 320, 320, True)

@@ -16,14 +16,15 @@ L.sdx_kernel_gemm_probe.argtypes = [C.c_int]
 
 def probe(label, make, flops):
     res = []
-    for mode in (0, 1, 2):
+    for mode in (0, 1, 2, 4):
         L.sdx_kernel_gemm_probe(mode)
         h = vp()
         assert make(C.byref(h)) == 0, L.sdx_kernel_last_error()
         res.append(time_plan(h))
         L.sdx_kernel_plan_destroy(h)
     L.sdx_kernel_gemm_probe(0)
-    print(f"{label:48s} full {res[0]:7.1f} us ({flops / res[0] / 1e6:6.1f} TF/s) | tma-only {res[1]:7.1f} | mma-only {res[2]:7.1f}",
+    print(f"{label:48s} full {res[0]:7.1f} us ({flops / res[0] / 1e6:6.1f} TF/s) | tma-only {res[1]:7.1f} | mma-only {res[2]:7.1f}"
+          f" | no-epilogue {res[3]:7.1f}",
           flush=True)
 
 
@@ -45,6 +46,10 @@ def gemm(M, N, K, bn, s=1):
                                             0, bn, s, hp), 2.0 * M * N * K)
 
 
+if len(sys.argv) > 1 and sys.argv[1] == "taesd":  # halo-tiled 64 -> 64 convs
+    for imgs, H in ((1, 512), (8, 512), (1, 256), (8, 256), (1, 128)):
+        conv(imgs, H, 64, 64, 0)
+    sys.exit(0)
 if len(sys.argv) > 1 and sys.argv[1] == "bn":
     for bn in (64, 96, 128, 160, 192, 224, 256, -128, -160, -256):
         gemm(8192, 8192, 4096, bn)

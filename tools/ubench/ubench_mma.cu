@@ -28,7 +28,7 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
                  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int VARIANT, int TS, int N>
+template <int VARIANT, int TS, int N, int AOFF = 0>
 __global__ void __launch_bounds__(128, 1) mma_kernel(long long* out, int n_mma) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(long long* out, int n_mma) 
     tc_fence_after();
     const uint32_t tmem = *slot;
     constexpr uint32_t idesc = idesc_bf16(128, N);
-    const uint64_t da = desc_kmajor_sw128(smem_u32(sA));
+    const uint64_t da = desc_kmajor_sw128(smem_u32(sA) + AOFF * 128);  // AOFF: A window start row (halo conv taps)
     const uint64_t db = desc_kmajor_sw128(smem_u32(sB));
     long long t0 = 0, t1 = 0, t2 = 0;
     if (warp == 0) {
@@ -82,10 +82,10 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(long long* out, int n_mma) 
     if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 
-template <int V, int TS, int N>
+template <int V, int TS, int N, int AOFF = 0>
 void run(long long* d, const char* name) {
     const int n_mma = 2048;
-    auto k = mma_kernel<V, TS, N>;
+    auto k = mma_kernel<V, TS, N, AOFF>;
     const int smem = 1024 + 16384 + 32768 + 64;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k<<<148, 128, smem>>>(d, n_mma);
@@ -104,6 +104,10 @@ void run(long long* d, const char* name) {
 int main() {
     long long* d;
     cudaMalloc(&d, 296 * sizeof(long long));
+    run<1, 0, 64, 1>(d, "SS warp+elect A at row 1");
+    run<1, 0, 64, 3>(d, "SS warp+elect A at row 3");
+    run<1, 0, 64, 8>(d, "SS warp+elect A at row 8");
+    run<1, 0, 128, 1>(d, "SS warp+elect A at row 1");
     run<1, 0, 16>(d, "SS warp+elect");
     run<1, 0, 32>(d, "SS warp+elect");
     run<0, 0, 64>(d, "SS lane0-divergent");
