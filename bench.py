@@ -73,7 +73,7 @@ class Dist:
             import torch.distributed as dist
 
             if backend == "nccl":
-                torch.cuda.set_device(self.local)
+                torch.cuda.set_device(int(os.environ.get("SDX_BENCH_DEVICE", self.local)))
             dist.init_process_group(backend)
             self.pg = dist
 
@@ -203,7 +203,9 @@ def run_ours(args, dist: Dist):
     from paper_2312_12491_b200 import _lib as L
     from paper_2312_12491_b200 import stagger as sg
 
-    dev = dist.local
+    # SDX_BENCH_DEVICE pins every rank to one GPU (a smoke test of the N > 1 path on a one-GPU
+    # box; the value is then not a scaling number)
+    dev = int(os.environ.get("SDX_BENCH_DEVICE", dist.local))
     S = args.streams
     cfg = workload_cfg(args)
     ring = 4
@@ -409,7 +411,7 @@ def main():
                 "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
-    dist = Dist("nccl" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "none")
+    dist = Dist(os.environ.get("SDX_BENCH_DIST_BACKEND", "nccl") if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "none")
     line = run_ours(args, dist)
     if dist.rank == 0:
         if not args.no_cpu_baseline and dist.world == 1:
