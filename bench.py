@@ -376,15 +376,19 @@ def cpu_reference(args, seconds: float, steps: int = 1, warmup: int = 0):
     frames = max(args.n_steps + 1, int(seconds / per_frame / max(1, steps)))
     ctx = mp.get_context("fork")
     vals = []
+    els = []
     with ctx.Pool(cores) as pool:
         for i in range(warmup + steps):
+            # warm-up steps run a short sample (they only warm the pool and caches)
+            nf = frames if i >= warmup else max(args.n_steps + 1, frames // 8)
             t = time.perf_counter()
-            res = pool.map(_cpu_worker, [(frames, d, args.n_steps, args.guidance, 7 + c) for c in range(cores)])
+            res = pool.map(_cpu_worker, [(nf, d, args.n_steps, args.guidance, 7 + c) for c in range(cores)])
             el = time.perf_counter() - t
             if i >= warmup:
                 vals.append(sum(r[0] for r in res) / el)
+                els.append(el)
     v = float(np.mean(vals))
-    return {"value": round(v, 3), "unit": "frames/s", "cores": cores,
+    return {"value": round(v, 3), "unit": "frames/s", "cores": cores, "ms_per_step": 1e3 * float(np.mean(els)),
             "kind": "reference" if which == "ref" else "port",
             "sample": (f"{cores} processes x {frames} frames of 3x512x512 (fp64 payload, identity codec: the "
                        f"reference has no UNet/TAESD), run_pipeline deterministic, n={args.n_steps} {args.guidance}, "
@@ -401,13 +405,23 @@ def main():
         if rank != 0:
             return
         steps = max(1, args.steps)
-        warm = max(0, min(args.warmup, 1))
-        budget = min(20.0, 150.0 / (steps + warm))
+        warm = max(0, args.warmup)
+        budget = min(20.0, 150.0 / (steps + warm / 8.0))  # CPU seconds per timed step (warm-up steps: 1/8)
         cb = cpu_reference(args, budget * steps, steps=steps, warmup=warm)
+        ms_step = cb.pop("ms_per_step")
+        # the same workload shape as our arm's line (streams, steps, guidance, frames); the
+        # reference computes it with its own analytic denoiser and identity codec (it has no
+        # UNet or TAESD), one stream per host core
+        config = {"workload": (f"img2img Stream Batch, {args.streams} stream(s) x {args.n_steps}-step "
+                               f"{args.guidance}, 3x512x512 frames, SSF eta 0.98 "
+                               f"{'off' if args.no_ssf else 'on'}: the reference's CPU run_pipeline"),
+                  "streams_per_gpu": args.streams, "n_steps": args.n_steps, "guidance": args.guidance,
+                  "frame": "3x512x512 u8", "reference_denoiser": "analytic Gaussian model (no UNet in the reference)",
+                  "reference_codec": "identity (no TAESD in the reference)", "host_streams": cb["cores"]}
         line = {"impl": "reference", "metric": "frames/s (img2img 512^2, 1-4 steps)", "value": cb["value"],
-                "unit": "frames/s", "n_gpus": 0, "steps": steps, "warmup": warm, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": cb["sample"]}, "cpu_baseline": cb,
+                "unit": "frames/s", "n_gpus": 0, "steps": steps, "warmup": warm, "ms_per_step": round(ms_step, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": config, "cpu_baseline": cb,
                 "e2e": {"value": cb["value"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -415,7 +429,9 @@ def main():
     line = run_ours(args, dist)
     if dist.rank == 0:
         if not args.no_cpu_baseline and dist.world == 1:
-            line["cpu_baseline"] = cpu_reference(args, args.cpu_seconds)
+            cb = cpu_reference(args, args.cpu_seconds)
+            cb.pop("ms_per_step", None)
+            line["cpu_baseline"] = cb
         print(json.dumps(line))
     dist.close()
 
