@@ -46,6 +46,9 @@ int sdx_kernel_attention(const void* q, int64_t q_rows_total, int64_t ld_q, int 
                          int64_t kv_rows_total, int64_t ld_kv, int k_col0, int v_col0, void* out, int64_t ld_out,
                          int images, int heads, int q_len, int kv_len, int kv_rows_per_img, const int* kv_index,
                          float scale, void* stream);
+/* Device buffer [images * cluster][8] int64 that subsequent cluster GroupNorm launches fill with
+ * per-CTA %globaltimer phase stamps; null disables (kernel benchmarks only). */
+int sdx_kernel_groupnorm_debug(void* dbg);
 const char* sdx_kernel_last_error(void);
 
 /* Prebuilt GEMM / conv launches for kernel benchmarks: plan once (tensor maps,

@@ -87,6 +87,10 @@ int sdx_kernel_conv3x3(const void* x, int imgs, int H, int W, int Cin, const voi
     });
 }
 
+int sdx_kernel_groupnorm_debug(void* dbg) {
+    return kguard([&] { sdx::set_groupnorm_debug_buffer(static_cast<long long*>(dbg)); });
+}
+
 int sdx_kernel_groupnorm(const void* x1, int C1, const void* x2, int C2, int HW, int imgs, float eps,
                          const float* gamma, const float* beta, int silu, void* out, void* arena, int iters,
                          void* stream) {

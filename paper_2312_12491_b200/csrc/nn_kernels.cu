@@ -337,6 +337,15 @@ __global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
     __shared__ float gpart[64];  // this CTA's (sum, sum of squares) per group
     __shared__ float st[32][2];
     pdl_launch();
+    long long* dbg = (p.dbg && threadIdx.x == 0) ? p.dbg + (blockIdx.y * gridDim.x + blockIdx.x) * 8 : nullptr;
+    auto stamp = [&](int i) {
+        if (dbg) {
+            long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : : "memory");
+            dbg[i] = t;
+        }
+    };
+    stamp(0);
     const int img = blockIdx.y;
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
@@ -358,6 +367,7 @@ __global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
     }
     __syncthreads();
     pdl_wait();
+    stamp(1);
     if (p.rows_dev && img >= *p.rows_dev) return;  // the whole cluster shares the image
     // load sequence number L: buffer L & 1, parity (L >> 1) & 1; phase A loads the
     // pieces as L = 0 .. np-1, a non-resident phase B again as L = np .. 2np-1
@@ -387,6 +397,7 @@ __global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
     float as[8] = {}, aq[8] = {};
     for (int i = 0; i < np; ++i) {
         gn_mbar_wait(&bar[i & 1], (i >> 1) & 1);
+        if (i == 0) stamp(2);
         const uint8_t* buf = gbuf + (i & 1) * kGnBufBytes;
         const int n = min(P, px1 - (px0 + i * P));
         const uint8_t* q = octet_ptr(buf, n, py);
@@ -427,7 +438,9 @@ __global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
         gpart[2 * g] = a;
         gpart[2 * g + 1] = b;
     }
+    stamp(3);
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    stamp(4);
     if (threadIdx.x < p.groups) {
         const int g = threadIdx.x;
         // all ranks' partials requested at once (independent DSMEM loads, <= 16 ranks), then
@@ -455,6 +468,7 @@ __global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
     // remote reads issued: release the partials (the matching wait is at exit)
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
     __syncthreads();
+    stamp(5);
     const float m0 = st[g0][0], r0 = st[g0][1];
     const float m1 = split < 8 ? st[g0 + 1][0] : 0.f, r1 = split < 8 ? st[g0 + 1][1] : 0.f;
     float sc[8], sh[8];
@@ -490,7 +504,9 @@ __global__ void __launch_bounds__(320, 1) gn_cluster_kernel(GnPlan p) {
             if (threadIdx.x == 0) issue(L + 2, i + 2);
         }
     }
+    stamp(6);
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    stamp(7);
 }
 
 // ---- LayerNorm (one warp per row) ------------------------------------------------
@@ -1063,7 +1079,14 @@ GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, in
 
 void free_groupnorm(GnPlan&) {}
 
-void run_groupnorm(const GnPlan& p, cudaStream_t st) {
+namespace {
+long long* g_gn_dbg = nullptr;
+}
+void set_groupnorm_debug_buffer(long long* dbg) { g_gn_dbg = dbg; }
+
+void run_groupnorm(const GnPlan& p_in, cudaStream_t st) {
+    GnPlan p = p_in;
+    p.dbg = g_gn_dbg;
     const int Ct = p.C1 + p.C2;
     const int noct = Ct / 8;
     if (p.cluster) {

@@ -35,6 +35,7 @@ struct GnPlan {
     // single launch, one thread-block cluster of `cluster` CTAs per image (DSMEM
     // statistics), pixel ranges streamed through shared memory in `piece`-pixel pieces
     int cluster, piece;
+    long long* dbg = nullptr;  // cluster kernel phase stamps [img * cluster + rank][8] (kernel benchmarks)
 };
 GnPlan plan_groupnorm(const bf16* x1, int C1, const bf16* x2, int C2, int HW, int imgs, float eps, const float* gamma,
                       const float* beta, int silu, bf16* out, const int* rows_dev, unsigned long long* acc,
@@ -43,6 +44,10 @@ void run_groupnorm(const GnPlan& p, cudaStream_t st);
 // one pass of the pair (0 statistics, 1 apply), for timing
 void run_groupnorm_part(const GnPlan& p, int part, cudaStream_t st);
 void free_groupnorm(GnPlan& p);
+// Device buffer that subsequent cluster GroupNorm launches fill with per-CTA %globaltimer
+// phase stamps (entry, after the PDL wait, first piece landed, statistics summed, cluster
+// barrier, group statistics, apply done, exit); null disables.  Kernel benchmarks only.
+void set_groupnorm_debug_buffer(long long* dbg);
 
 // LayerNorm over the last dim C of [rows][C] (fp32 stats), bf16 out.
 void run_layernorm(const bf16* x, int rows, int C, const float* gamma, const float* beta, float eps, bf16* out,
