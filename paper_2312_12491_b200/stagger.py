@@ -402,14 +402,13 @@ class Pipeline:
 
     def pop_all(self, stream: int):
         out = []
-        buf = np.empty(self.out_bytes, dtype=np.uint8)
         seq, has = C.c_int64(), C.c_int()
         while True:
+            buf = np.empty(self.out_bytes, dtype=np.uint8)  # popped into directly (one host copy)
             _check(L.lib.sdx_pipeline_pop(self._h, stream, C.byref(seq), buf.ctypes.data, C.byref(has)))
             if not has.value:
                 return out
-            payload = buf.copy() if self.out_is_u8 else buf.view(np.float32).copy()
-            out.append((seq.value, payload))
+            out.append((seq.value, buf if self.out_is_u8 else buf.view(np.float32)))
 
     def report(self, stream: int = 0) -> dict:
         r = L.sdx_report()
