@@ -288,16 +288,18 @@ def run_ours(args, dist: Dist):
         algo = S * rpf * unet_flops  # FLOPs of one batched UNet call (steady state)
         achieved = algo / (den_ms * 1e-3) / 1e12
         peak = peaks.get("bf16_tflops_sustained", 1400.0)
-        traffic = None  # DRAM bytes of one UNet forward at this row count, from a committed ncu capture
+        traffic, traffic_detail = None, None  # DRAM bytes of one UNet forward at this row count (ncu capture)
         for tf in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_unet_traffic.json"))):
             td = json.load(open(tf))
             if td.get("rows") == S * rpf:
-                traffic = {"dram_bytes_per_launch": td["dram_bytes"], "read": td["dram_bytes_read"],
-                           "write": td["dram_bytes_write"], "source": os.path.relpath(tf, ROOT)}
+                traffic = td["dram_bytes"]
+                traffic_detail = {"read": td["dram_bytes_read"], "write": td["dram_bytes_write"],
+                                  "source": os.path.relpath(tf, ROOT)}
         roof = {"bound": "tensor", "kernel": "UNet forward (tcgen05 conv/GEMM + flash-attention kernels), "
                                               f"{S * rpf} rows/launch",
                 "achieved": round(achieved, 2), "peak": peak, "unit": "TFLOP/s", "frac": round(achieved / peak, 4),
-                "traffic": traffic, "algo_flops_per_launch": algo, "avg_launch_ms": round(den_ms, 4),
+                "traffic": traffic, "traffic_detail": traffic_detail, "algo_flops_per_launch": algo,
+                "avg_launch_ms": round(den_ms, 4),
                 "peak_source": "MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS, long loop)"}
         frame_flops = rpf * unet_flops + codec_flops
         workload = (f"img2img Stream Batch, {S} stream(s)/GPU x {cfg.n_steps}-step {cfg.guidance_mode}, "
