@@ -285,15 +285,20 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                 const int s = it % STAGES;
                 wait_bounded(&full[s], (it / STAGES) & 1);
                 tc_fence_after();
-                const uint32_t abase = smem_u32(sA + s * A_BYTES);
-#pragma unroll 1
+                // descriptors: the A window of a tap is the stage's box shifted by whole 128-byte
+                // rows, and the start address sits in the descriptor's low bits (16-byte units), so
+                // every tap's descriptor is the base one plus a constant; the fully unrolled tap
+                // loop issues the 36 MMAs back to back
+                const uint64_t da0 = desc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
+                const uint64_t db0 = desc_kmajor_sw128(smem_u32(sB));
+#pragma unroll
                 for (int tap = 0; tap < 9; ++tap) {
                     const int dy = tap / 3, dx = tap - dy * 3;
                     // output pixel i of the tile reads halo pixel (dy, i + dx): 128 consecutive rows
                     // the SW128 XOR pattern follows the absolute smem address bits (as the TMA wrote
                     // it), so a start at any 128-byte row needs no descriptor base offset
-                    const uint64_t da = desc_kmajor_sw128(abase + static_cast<uint32_t>(dy * 130 + dx) * 128);
-                    const uint64_t db = desc_kmajor_sw128(smem_u32(sB + tap * B_BYTES));
+                    const uint64_t da = da0 + static_cast<uint64_t>((dy * 130 + dx) * 128 / 16);
+                    const uint64_t db = db0 + static_cast<uint64_t>(tap * B_BYTES / 16);
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
                         umma_f16_el(dtm, da + 2 * k, db + 2 * k, idesc, (tap != 0 || k != 0) ? 1u : 0u);
@@ -379,6 +384,8 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
             constexpr uint32_t idesc = idesc_bf16(PAIR ? 2 * BM : BM, BN);
             uint32_t it = 0, lt = 0, ph = 0;
             int s = 0;  // stage ring position (advanced incrementally, as the producer's)
+            // stage descriptors = stage-0 descriptors + the stage offset (16-byte units)
+            const uint64_t da0 = desc_kmajor_sw128(smem_u32(sA)), db0 = desc_kmajor_sw128(smem_u32(sB));
             for (int u = ustart; u < total; u += ustep, ++lt) {
                 const int sp = u % splits;
                 const int kb0 = sp * nk / splits, kb1 = (sp + 1) * nk / splits;
@@ -390,8 +397,8 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
                     wait_bounded(&full[s], ph);
                     if (dbg && it == 0 && lane == 0) dbg[2] = gtimer();
                     tc_fence_after();
-                    const uint64_t da = desc_kmajor_sw128(smem_u32(sA + s * A_BYTES));
-                    const uint64_t db = desc_kmajor_sw128(smem_u32(sB + s * B_BYTES));
+                    const uint64_t da = da0 + static_cast<uint64_t>(s) * (A_BYTES >> 4);
+                    const uint64_t db = db0 + static_cast<uint64_t>(s) * (B_BYTES >> 4);
 #pragma unroll
                     for (int k = 0; k < (g.xmode == 1 ? 0 : BK / 16); ++k) {  // +32 B per K=16 step in the swizzle atom
                         if (PAIR) umma_f16_pair_el(dtm, da + 2 * k, db + 2 * k, idesc, (kb != kb0 || k != 0) ? 1u : 0u);
