@@ -35,10 +35,18 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(long long* out, int n_mma) 
     uint8_t* sA = sm;            // 128 x 64 bf16, sw128 (16 KB)
     uint8_t* sB = sm + 16384;    // 256 x 64 bf16 (32 KB)
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 16384 + 32768);
-    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint64_t* ready = bar + 1;  // VARIANT 2: a completed barrier polled before every 4 MMAs
+    uint64_t* sink = bar + 2;   // VARIANT 2: committed after every 4 MMAs (never completes)
+    uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 3);
     for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) { mbar_init(bar, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(ready, 1);
+        mbar_init(sink, 1 << 19);
+        fence_barrier_init();
+        mbar_arrive(ready);  // phase 0 complete
+    }
     if (warp == 0) tmem_alloc(slot, 512);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     tc_fence_before();
@@ -63,6 +71,21 @@ __global__ void __launch_bounds__(128, 1) mma_kernel(long long* out, int n_mma) 
                 mbar_wait(bar, 0);
                 t2 = clock64();
             }
+        } else if (VARIANT == 2) {
+            // the GEMM mainloop's per-stage skeleton: poll a (ready) full barrier, fence, 4 MMAs,
+            // commit the stage's empty barrier
+            t0 = clock64();
+            for (int i = 0; i < n_mma; i += 4) {
+                mbar_wait(ready, 0);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < 4; ++k) umma_ss_elect(tmem, da + 2 * k, db + 2 * k, idesc, (i + k) > 0);
+                commit_elect(sink);
+            }
+            t1 = clock64();
+            commit_elect(bar);
+            mbar_wait(bar, 0);
+            t2 = clock64();
         } else {
             t0 = clock64();
             for (int i = 0; i < n_mma; ++i) {
@@ -104,6 +127,11 @@ void run(long long* d, const char* name) {
 int main() {
     long long* d;
     cudaMalloc(&d, 296 * sizeof(long long));
+    run<2, 0, 64>(d, "SS GEMM stage skeleton (wait/fence/4/commit)");
+    run<2, 0, 96>(d, "SS GEMM stage skeleton (wait/fence/4/commit)");
+    run<2, 0, 160>(d, "SS GEMM stage skeleton (wait/fence/4/commit)");
+    run<2, 0, 256>(d, "SS GEMM stage skeleton (wait/fence/4/commit)");
+    run<1, 0, 96>(d, "SS warp+elect");
     run<1, 0, 64, 1>(d, "SS warp+elect A at row 1");
     run<1, 0, 64, 3>(d, "SS warp+elect A at row 3");
     run<1, 0, 64, 8>(d, "SS warp+elect A at row 8");
