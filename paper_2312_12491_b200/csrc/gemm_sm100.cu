@@ -142,16 +142,20 @@ __device__ __forceinline__ void gn_sink_chunk(const GemmEpilogue& e, int ngn, co
 // own epilogue.  Halves the per-SM B traffic (L2 and smem) of a 256 x BN tile.
 // Epilogue warps: 12 (3 per TMEM lane quadrant, 2 KB smem box each) on the fast path,
 // whose small-K GEMMs are epilogue-bound; 8 (4 KB fp32 slabs) on the general path.
-template <bool FAST>
+// The halo conv (TAESD, N = 64) runs its fast epilogue with 8 warps: the CTA's warps spread over
+// the SM's 4 sub-partitions, whose register files bound the registers per thread (14 warps: 128,
+// with spills; 10 warps: 168, none).  Measured: TAESD encode / decode 4-5% faster, while the
+// UNet's K = 320 GEMMs keep the 12 warps they need (8 warps: 0.6% slower per forward).
+template <bool FAST, bool HALO = false>
 struct EpiCfg {
     static_assert(kRowStatParts * 4 == 12, "row-statistics partials = fast-path epilogue warps per quadrant");
-    static constexpr int kWarps = FAST ? 12 : 8;
+    static constexpr int kWarps = FAST && !HALO ? 12 : 8;
     static constexpr int kSlab = FAST ? 2048 : 4096;
     static constexpr int kThreads = 64 + 32 * kWarps;
 };
 
 template <int BN, int STAGES, int AMODE, bool FAST, bool PAIR>
-__global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
+__global__ void __launch_bounds__(EpiCfg<FAST, AMODE == kAHalo>::kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap ta2,
                    const __grid_constant__ CUtensorMap tb, const __grid_constant__ CUtensorMap to, const GemmArgs g) {
     static_assert(!PAIR || FAST, "CTA-pair GEMM uses the fast epilogue");
@@ -170,7 +174,7 @@ __global__ void __launch_bounds__(EpiCfg<FAST>::kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    constexpr int NEPI = EpiCfg<FAST>::kWarps, SLAB = EpiCfg<FAST>::kSlab;
+    constexpr int NEPI = EpiCfg<FAST, AMODE == kAHalo>::kWarps, SLAB = EpiCfg<FAST, AMODE == kAHalo>::kSlab;
     uint8_t* slabs = sB + (HALO ? 9 : STAGES) * B_BYTES;  // NEPI epilogue warps x SLAB (1024-aligned)
     uint64_t* full = reinterpret_cast<uint64_t*>(slabs + NEPI * SLAB);
     uint64_t* empty = full + STAGES;
@@ -1087,14 +1091,14 @@ template <int BN, bool PAIR, int AMODE, bool FAST>
 constexpr int stages_for() {
     if (AMODE == kAHalo) return 2;  // 2 x 49 KB halo boxes next to 72 KB of resident weights
     constexpr int bnl = PAIR ? BN / 2 : BN;
-    constexpr int slabs = EpiCfg<FAST>::kWarps * EpiCfg<FAST>::kSlab;
+    constexpr int slabs = EpiCfg<FAST, AMODE == kAHalo>::kWarps * EpiCfg<FAST, AMODE == kAHalo>::kSlab;
     constexpr int st = (232448 - 1024 - slabs - 256) / (128 * 64 * 2 + bnl * 64 * 2);
     return st > 8 ? 8 : st;
 }
 
 template <int BN, bool PAIR, int AMODE, bool FAST>
 size_t smem_for() {
-    constexpr int slabs = EpiCfg<FAST>::kWarps * EpiCfg<FAST>::kSlab;
+    constexpr int slabs = EpiCfg<FAST, AMODE == kAHalo>::kWarps * EpiCfg<FAST, AMODE == kAHalo>::kSlab;
     if (AMODE == kAHalo) return 1024 + 2 * 50176 + 9 * BN * 64 * 2 + slabs + 256;
     constexpr int bnl = PAIR ? BN / 2 : BN;
     return 1024 + static_cast<size_t>(stages_for<BN, PAIR, AMODE, FAST>()) * (128 * 64 * 2 + bnl * 64 * 2) + slabs + 256;
@@ -1136,7 +1140,7 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
         const int np = pairs < kSmCount / 2 ? pairs : kSmCount / 2;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * np);
-        cfg.blockDim = dim3(EpiCfg<FAST>::kThreads);
+        cfg.blockDim = dim3(EpiCfg<FAST, AMODE == kAHalo>::kThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cudaLaunchAttribute at[2];
@@ -1152,7 +1156,7 @@ void launch_t(const GemmPlan& p, cudaStream_t st) {
     } else {
         const int units = n_tiles * ((p.M + 127) / 128) * p.splits;
         dim3 grid(units < kSmCount ? units : kSmCount);
-        launch_pdl(k, grid, dim3(EpiCfg<FAST>::kThreads), smem, st, p.ta, p.ta2, p.tb, p.to, g);
+        launch_pdl(k, grid, dim3(EpiCfg<FAST, AMODE == kAHalo>::kThreads), smem, st, p.ta, p.ta2, p.tb, p.to, g);
     }
     if (p.splits > 1) {
         const long long work = static_cast<long long>(p.M) * ((p.N + 7) / 8);
